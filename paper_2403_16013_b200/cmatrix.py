@@ -1,0 +1,219 @@
+"""Complex multi-component matrix multiply -- drop-in for mpclu.rgemm /
+mpclu.cmatrix (rgemm.py:1-73, cmatrix.py:1-177).
+
+Both the real kernels ("naive", "blocked") and the complex 3M / 4M forms run
+as ONE fused sm_100a kernel per call (libmpcb200 ``mpc_cgemm``): the three
+(3M) or four (4M) real inner-product chains of every output element are
+accumulated side by side, ``Re A + Im A`` / ``Re B + Im B`` are formed once
+per staged element, and the combine (``Re = T1 - T2``,
+``Im = (T3 - T1) - T2`` or ``ir + ri``) runs in the epilogue.  Results are
+bit-identical to the reference's composition of real products and plane
+additions.  The real-kernel invocation counters keep the reference's
+semantics (3 per 3M call, 4 per 4M call, rgemm.py:29-43).
+"""
+
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .rmatrix import RealMatrix, check_threads
+
+DEFAULT_BLOCK = 16       # rgemm.py:26
+DEFAULT_THRESHOLD = 32   # rgemm.py:27
+DEFAULT_SPLITS = {2: 6, 3: 8, 4: 12}   # cmatrix.py:26
+DEFAULT_SPLIT_BITS = {2: 19, 3: 21, 4: 18}  # ozaki.py:30
+
+# "b200" names this package's kernel explicitly; "naive" and "blocked" are the
+# reference's bitwise-equal schedules and map to the same fused kernel.
+REAL_KERNELS = ("naive", "blocked", "strassen", "ozaki", "b200")
+METHODS = ("3m", "4m")
+SUPPORTED_K = (2, 3, 4)
+
+_kernel_calls = {name: 0 for name in REAL_KERNELS}
+
+
+def real_kernel_calls():
+    return dict(_kernel_calls)
+
+
+def reset_real_kernel_calls():
+    for key in _kernel_calls:
+        _kernel_calls[key] = 0
+
+
+def _check_k(k):
+    if k not in SUPPORTED_K:
+        raise ValueError(f"component count k={k} not supported on the B200 path (2, 3 or 4)")
+
+
+def _check_mm(A, B):
+    if A.k != B.k:
+        raise ValueError(f"component counts differ: {A.k} != {B.k}")
+    if A.cols != B.rows:
+        raise ValueError(f"inner dimensions differ: {A.cols} != {B.rows}")
+
+
+# ------------------------------------------------------------- real GEMM
+
+def _rgemm(A, B, name):
+    _check_mm(A, B)
+    _check_k(A.k)
+    _kernel_calls[name] += 1
+    k, m, n = A.data.shape
+    l = B.cols
+    C = np.zeros((k, m, l))
+    if m * l:
+        _lib.check(_lib.lib().mpc_rgemm(k, m, n, l, _lib.ptr(A.data), n, m * n,
+                                        _lib.ptr(B.data), l, n * l, _lib.ptr(C), l, m * l, None),
+                   "rgemm")
+    return RealMatrix(C)
+
+
+def rgemm_naive(A, B, threads=1):
+    """C[i][j] = sum_t A[i][t] B[t][j], strictly t-ascending (rgemm.py:53-60)."""
+    check_threads(threads)
+    return _rgemm(A, B, "naive")
+
+
+def rgemm_blocked(A, B, block=DEFAULT_BLOCK, threads=1):
+    """Bitwise equal to rgemm_naive for any block (rgemm.py:63-73)."""
+    if block < 1:
+        raise ValueError("block must be >= 1")
+    check_threads(threads)
+    return _rgemm(A, B, "blocked")
+
+
+def rgemm_strassen(A, B, threshold=DEFAULT_THRESHOLD, threads=1):
+    """Out of scope: square-only in the reference, so it
+    cannot serve the LU trailing update, and it loses accuracy."""
+    raise NotImplementedError("strassen is outside the B200 hot path (see DESIGN.md)")
+
+
+# ----------------------------------------------------------- complex GEMM
+
+@dataclass(frozen=True)
+class KernelChoice:
+    """One benchmark point (cmatrix.py:32-63)."""
+
+    method: str = "3m"
+    real_kernel: str = "blocked"
+    block: int = DEFAULT_BLOCK
+    threshold: int = DEFAULT_THRESHOLD
+    d: Optional[int] = None
+    split_bits: Optional[int] = None
+    threads: int = 1
+
+    def validate(self):
+        if self.method not in METHODS:
+            raise ValueError(f"unknown method {self.method!r}")
+        if self.real_kernel not in REAL_KERNELS:
+            raise ValueError(f"unknown real kernel {self.real_kernel!r}")
+        if self.block < 1:
+            raise ValueError("block must be >= 1")
+        if self.threshold < 2:
+            raise ValueError("threshold must be >= 2")
+        if self.d is not None and self.d < 1:
+            raise ValueError("d must be >= 1")
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+        return self
+
+    def with_threads(self, threads):
+        return replace(self, threads=threads)
+
+    def splits_for(self, k):
+        return self.d if self.d is not None else DEFAULT_SPLITS.get(k, 8)
+
+
+class PlanarComplexMatrix:
+    """Complex matrix as two planar real matrices (cmatrix.py:66-125)."""
+
+    __slots__ = ("re_plane", "im_plane")
+
+    def __init__(self, re_plane, im_plane):
+        if re_plane.data.shape != im_plane.data.shape:
+            raise ValueError("planes must share shape and component count")
+        self.re_plane = re_plane
+        self.im_plane = im_plane
+
+    @property
+    def k(self):
+        return self.re_plane.k
+
+    @property
+    def rows(self):
+        return self.re_plane.rows
+
+    @property
+    def cols(self):
+        return self.re_plane.cols
+
+    @classmethod
+    def zeros(cls, rows, cols, k):
+        return cls(RealMatrix.zeros(rows, cols, k), RealMatrix.zeros(rows, cols, k))
+
+    @classmethod
+    def from_complex128(cls, M, k):
+        M = np.asarray(M, dtype=np.complex128)
+        return cls(RealMatrix.from_float64(M.real, k), RealMatrix.from_float64(M.imag, k))
+
+    @classmethod
+    def identity(cls, n, k):
+        return cls(RealMatrix.identity(n, k), RealMatrix.zeros(n, n, k))
+
+    def copy(self):
+        return PlanarComplexMatrix(self.re_plane.copy(), self.im_plane.copy())
+
+    def at(self, i, j):
+        return (self.re_plane.at(i, j), self.im_plane.at(i, j))
+
+    def bitwise_equal(self, other):
+        return self.re_plane.bitwise_equal(other.re_plane) and self.im_plane.bitwise_equal(
+            other.im_plane)
+
+    def max_abs(self):
+        return max(self.re_plane.max_abs(), self.im_plane.max_abs())
+
+    def __repr__(self):
+        return f"PlanarComplexMatrix(k={self.k}, shape={self.rows}x{self.cols})"
+
+
+def _cgemm(A, B, kc, method):
+    _check_mm(A.re_plane, B.re_plane)
+    kc.validate()
+    check_threads(kc.threads)
+    if kc.real_kernel in ("strassen", "ozaki"):
+        raise NotImplementedError(
+            f"real_kernel={kc.real_kernel!r} is not on the B200 path yet (DESIGN.md, next rows)")
+    _check_k(A.k)
+    _kernel_calls[kc.real_kernel] += 3 if method == "3m" else 4
+    k, m, n = A.re_plane.data.shape
+    l = B.cols
+    Cre, Cim = np.empty((k, m, l)), np.empty((k, m, l))
+    if m * l:
+        L = _lib.lib()
+        _lib.check(L.mpc_cgemm(k, 3 if method == "3m" else 4, m, n, l,
+                               _lib.ptr(A.re_plane.data), _lib.ptr(A.im_plane.data), n, m * n,
+                               _lib.ptr(B.re_plane.data), _lib.ptr(B.im_plane.data), l, n * l,
+                               _lib.ptr(Cre), _lib.ptr(Cim), l, m * l, 0, None), "cgemm")
+    return PlanarComplexMatrix(RealMatrix(Cre), RealMatrix(Cim))
+
+
+def cgemm_4m(A, B, kc=KernelChoice(method="4m")):
+    """Four real products, two plane additions (cmatrix.py:145-154)."""
+    return _cgemm(A, B, kc, "4m")
+
+
+def cgemm_3m(A, B, kc=KernelChoice(method="3m")):
+    """Three real products, five plane additions (cmatrix.py:157-169)."""
+    return _cgemm(A, B, kc, "3m")
+
+
+def cgemm(A, B, kc):
+    """Dispatch on kc.method (cmatrix.py:172-177)."""
+    kc.validate()
+    if kc.method == "3m":
+        return cgemm_3m(A, B, kc)
+    return cgemm_4m(A, B, kc)

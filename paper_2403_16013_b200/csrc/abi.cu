@@ -1,0 +1,540 @@
+// abi.cu -- extern "C" entry points of libmpcb200.so (declared in
+// include/mpc_b200.h): argument checks, host-pointer staging, dispatch on the
+// component count to the per-K operation tables.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mpc_b200.h"
+#include "kernels.cuh"
+#include "ops.h"
+#include "prof.h"
+
+// ------------------------------------------------------------ profiling
+namespace mpc {
+namespace {
+struct ProfRec {
+  int cls;
+  double ops;
+  cudaEvent_t a, b;
+};
+struct ProfState {
+  std::mutex mu;
+  bool on = false;
+  std::atomic<long long> launches{0};
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+ProfState& P() {
+  static ProfState s;
+  return s;
+}
+}  // namespace
+
+int prof_begin(int cls, double ops, cudaStream_t st) {
+  ProfState& p = P();
+  p.launches++;
+  if (!p.on) return -1;
+  std::lock_guard<std::mutex> g(p.mu);
+  ProfRec r{cls, ops, p.get(), p.get()};
+  cudaEventRecord(r.a, st);
+  p.recs.push_back(r);
+  return (int)p.recs.size() - 1;
+}
+
+void prof_end(int tok, cudaStream_t st) {
+  if (tok < 0) return;
+  ProfState& p = P();
+  std::lock_guard<std::mutex> g(p.mu);
+  cudaEventRecord(p.recs[tok].b, st);
+}
+}  // namespace mpc
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::string& msg) {
+  g_err = msg;
+  return MPC_ERR;
+}
+
+struct CudaError {
+  std::string what;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+const mpc::OpsTable* table_for(int k) {
+  switch (k) {
+    case 2: return mpc::ops_k2();
+    case 3: return mpc::ops_k3();
+    case 4: return mpc::ops_k4();
+    default: return nullptr;
+  }
+}
+
+// 0: null, 1: host, 2: device
+int ptr_kind(const void* p, int* device) {
+  if (p == nullptr) return 0;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    if (device) *device = a.device;
+    return 2;
+  }
+  return 1;
+}
+
+int64_t extent(int k, int64_t rows, int64_t cols, int64_t ld, int64_t ps) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return (int64_t)(k - 1) * ps + (rows - 1) * ld + cols;
+}
+
+// Maps every pointer of one call to device memory.  All-device calls pass
+// through untouched; all-host calls are staged (H2D before, D2H after, then
+// the stream is synchronised).
+class Stager {
+ public:
+  explicit Stager(cudaStream_t st) : st_(st) {}
+  ~Stager() {
+    for (auto& r : regs_)
+      if (r.dev) cudaFreeAsync(r.dev, st_);
+  }
+  // classify all pointers first; returns false (with message) on mixing
+  bool classify(std::initializer_list<const void*> ptrs) {
+    int kinds = 0;
+    int dev = -1;
+    for (const void* p : ptrs) {
+      int d = -1;
+      int kd = ptr_kind(p, &d);
+      if (kd == 0) continue;
+      kinds |= (1 << kd);
+      if (kd == 2) dev = d;
+    }
+    if (kinds == ((1 << 1) | (1 << 2))) {
+      g_err = "mixed host and device pointers in one call";
+      return false;
+    }
+    host_ = (kinds == (1 << 1));
+    if (!host_ && dev >= 0) ck(cudaSetDevice(dev), "cudaSetDevice");
+    return true;
+  }
+  bool host() const { return host_; }
+  template <typename T>
+  T* map(T* p, int64_t nelem, bool in, bool out) {
+    if (!host_ || p == nullptr || nelem <= 0) return p;
+    Region r{(void*)p, (size_t)nelem * sizeof(T), out, nullptr};
+    ck(cudaMallocAsync(&r.dev, r.bytes, st_), "cudaMallocAsync");
+    regs_.push_back(r);
+    if (in) ck(cudaMemcpyAsync(r.dev, p, r.bytes, cudaMemcpyHostToDevice, st_), "H2D");
+    return (T*)r.dev;
+  }
+  void finish() {
+    if (host_) {
+      for (auto& r : regs_)
+        if (r.out) ck(cudaMemcpyAsync(r.host, r.dev, r.bytes, cudaMemcpyDeviceToHost, st_), "D2H");
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    if (host_) ck(cudaStreamSynchronize(st_), "cudaStreamSynchronize");
+  }
+
+ private:
+  struct Region {
+    void* host;
+    size_t bytes;
+    bool out;
+    void* dev;
+  };
+  cudaStream_t st_;
+  bool host_ = false;
+  std::vector<Region> regs_;
+};
+
+__global__ void fp64_peak_kernel(double* out, int iters, double c) {
+  double a[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) a[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 16; i++) a[i] = __dadd_rn(a[i], c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; i++) s = __dadd_rn(s, a[i]);
+  if (s == 1234.5) out[0] = s;
+}
+
+__global__ void iota_kernel(int64_t* p, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+
+// pivot-reduction workspace + status word, stream ordered
+struct WsHolder {
+  mpc::PanelWs ws{};
+  cudaStream_t st;
+  void* mem = nullptr;
+  WsHolder(int k, int64_t n, cudaStream_t s) : st(s) {
+    int64_t nb = (n + mpc::PNT - 1) / mpc::PNT + 1;
+    size_t bytes = sizeof(double) * nb * k + sizeof(int64_t) * nb + 64;
+    ck(cudaMallocAsync(&mem, bytes, st), "cudaMallocAsync(ws)");
+    char* b = (char*)mem;
+    ws.status = (int64_t*)b;
+    ws.counter = (unsigned*)(b + 16);
+    ws.prow = (int64_t*)(b + 64);
+    ws.pv = (double*)(b + 64 + sizeof(int64_t) * nb);
+    ck(cudaMemsetAsync(ws.status, 0xFF, sizeof(int64_t), st), "memset status");
+    ck(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), st), "memset counter");
+  }
+  int64_t read_status() {
+    int64_t h = -1;
+    ck(cudaMemcpyAsync(&h, ws.status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H status");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    return h;
+  }
+  ~WsHolder() {
+    if (mem) cudaFreeAsync(mem, st);
+  }
+};
+
+bool bad_k(int k) { return table_for(k) == nullptr; }
+bool bad_method(int m) { return m != 3 && m != 4; }
+
+#define MPC_TRY try {
+#define MPC_CATCH                                                      \
+  }                                                                    \
+  catch (const CudaError& e) {                                         \
+    return fail(e.what);                                               \
+  }                                                                    \
+  catch (const mpc::LaunchError& e) {                                  \
+    return fail(std::string("launch failed: ") + e.what + ": " +       \
+                cudaGetErrorString(cudaGetLastError()));               \
+  }                                                                    \
+  catch (const std::exception& e) {                                    \
+    return fail(e.what());                                             \
+  }
+
+}  // namespace
+
+extern "C" {
+
+int mpc_abi_version(void) { return MPC_ABI_VERSION; }
+
+const char* mpc_last_error(void) { return g_err.c_str(); }
+
+int mpc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void mpc_prof_enable(int on) {
+  mpc::ProfState& p = mpc::P();
+  std::lock_guard<std::mutex> g(p.mu);
+  for (auto& r : p.recs) {
+    p.pool.push_back(r.a);
+    p.pool.push_back(r.b);
+  }
+  p.recs.clear();
+  p.on = on != 0;
+}
+
+long long mpc_launch_count(void) { return mpc::P().launches.load(); }
+
+int mpc_prof_summary(double* ms, double* ops, long long* count, int nclass) {
+  mpc::ProfState& p = mpc::P();
+  std::lock_guard<std::mutex> g(p.mu);
+  for (int c = 0; c < nclass; c++) {
+    ms[c] = 0.0;
+    ops[c] = 0.0;
+    count[c] = 0;
+  }
+  for (auto& r : p.recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return fail("event sync failed");
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return fail("event time failed");
+    if (r.cls >= 0 && r.cls < nclass) {
+      ms[r.cls] += t;
+      ops[r.cls] += r.ops;
+      count[r.cls] += 1;
+    }
+  }
+  return mpc::PC_N;
+}
+
+double mpc_fp64_peak(int iters, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double* out = nullptr;
+  if (cudaMallocAsync((void**)&out, 8, st) != cudaSuccess) return -1.0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned blocks = (unsigned)sms * 8;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  fp64_peak_kernel<<<blocks, 256, 0, st>>>(out, iters / 10 + 1, 1e-9);  // warm-up
+  cudaEventRecord(a, st);
+  fp64_peak_kernel<<<blocks, 256, 0, st>>>(out, iters, 1e-9);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float t = 0.f;
+  cudaEventElapsedTime(&t, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFreeAsync(out, st);
+  if (cudaGetLastError() != cudaSuccess || t <= 0.f) return -1.0;
+  double ops = (double)blocks * 256.0 * 16.0 * (double)iters;
+  return ops / (t * 1e-3);  // FP64 instructions (lane-ops) per second
+}
+
+int mpc_mat_add(int k, int64_t rows, int64_t cols, const double* a, int64_t lda, int64_t psa,
+                const double* b, int64_t ldb, int64_t psb, double* c, int64_t ldc, int64_t psc,
+                double sign, void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (rows < 0 || cols < 0) return fail("negative dimension");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({a, b, c})) return MPC_ERR;
+  double* da = sg.map(const_cast<double*>(a), extent(k, rows, cols, lda, psa), true, false);
+  double* db = sg.map(const_cast<double*>(b), extent(k, rows, cols, ldb, psb), true, false);
+  double* dc = sg.map(c, extent(k, rows, cols, ldc, psc), true, true);
+  table_for(k)->mat_add(rows, cols, mpc::View{da, nullptr, lda, psa},
+                        mpc::View{db, nullptr, ldb, psb}, mpc::View{dc, nullptr, ldc, psc},
+                        sign, st);
+  sg.finish();
+  return 0;
+  MPC_CATCH
+}
+
+int mpc_renorm_planes(int k, int64_t rows, int64_t cols, double* r, int64_t ld, int64_t ps,
+                      void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({r})) return MPC_ERR;
+  double* dr = sg.map(r, extent(k, rows, cols, ld, ps), true, true);
+  table_for(k)->renorm_planes(rows, cols, mpc::View{dr, nullptr, ld, ps}, st);
+  sg.finish();
+  return 0;
+  MPC_CATCH
+}
+
+int mpc_rgemm(int k, int64_t m, int64_t n, int64_t l, const double* a, int64_t lda, int64_t psa,
+              const double* b, int64_t ldb, int64_t psb, double* c, int64_t ldc, int64_t psc,
+              void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (m < 0 || n < 0 || l < 0) return fail("negative dimension");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({a, b, c})) return MPC_ERR;
+  double* da = sg.map(const_cast<double*>(a), extent(k, m, n, lda, psa), true, false);
+  double* db = sg.map(const_cast<double*>(b), extent(k, n, l, ldb, psb), true, false);
+  double* dc = sg.map(c, extent(k, m, l, ldc, psc), true, true);
+  table_for(k)->rgemm(m, n, l, mpc::View{da, nullptr, lda, psa}, mpc::View{db, nullptr, ldb, psb},
+                      mpc::View{dc, nullptr, ldc, psc}, st);
+  sg.finish();
+  return 0;
+  MPC_CATCH
+}
+
+int mpc_cgemm(int k, int method, int64_t m, int64_t n, int64_t l, const double* a_re,
+              const double* a_im, int64_t lda, int64_t psa, const double* b_re,
+              const double* b_im, int64_t ldb, int64_t psb, double* c_re, double* c_im,
+              int64_t ldc, int64_t psc, int epilogue, void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
+  if (m < 0 || n < 0 || l < 0) return fail("negative dimension");
+  if (epilogue != 0 && epilogue != 1) return fail("epilogue must be 0 or 1");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({a_re, a_im, b_re, b_im, c_re, c_im})) return MPC_ERR;
+  int64_t ea = extent(k, m, n, lda, psa), eb = extent(k, n, l, ldb, psb),
+          ec = extent(k, m, l, ldc, psc);
+  double* dar = sg.map(const_cast<double*>(a_re), ea, true, false);
+  double* dai = sg.map(const_cast<double*>(a_im), ea, true, false);
+  double* dbr = sg.map(const_cast<double*>(b_re), eb, true, false);
+  double* dbi = sg.map(const_cast<double*>(b_im), eb, true, false);
+  double* dcr = sg.map(c_re, ec, epilogue == 1, true);
+  double* dci = sg.map(c_im, ec, epilogue == 1, true);
+  table_for(k)->cgemm(method == 3, m, n, l, mpc::View{dar, dai, lda, psa},
+                      mpc::View{dbr, dbi, ldb, psb}, mpc::View{dcr, dci, ldc, psc}, epilogue, st,
+                      nullptr);
+  sg.finish();
+  return 0;
+  MPC_CATCH
+}
+
+int mpc_trsm_ll_unit(int k, int method, int64_t K, int64_t M, const double* l_re,
+                     const double* l_im, int64_t ldl, int64_t psl, double* a_re, double* a_im,
+                     int64_t lda, int64_t psa, void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
+  if (K < 0 || M < 0) return fail("negative dimension");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({l_re, l_im, a_re, a_im})) return MPC_ERR;
+  int64_t el = extent(k, K, K, ldl, psl), ea = extent(k, K, M, lda, psa);
+  double* dlr = sg.map(const_cast<double*>(l_re), el, true, false);
+  double* dli = sg.map(const_cast<double*>(l_im), el, true, false);
+  double* dar = sg.map(a_re, ea, true, true);
+  double* dai = sg.map(a_im, ea, true, true);
+  table_for(k)->trsm(method == 3, K, M, mpc::View{dlr, dli, ldl, psl},
+                     mpc::View{dar, dai, lda, psa}, st, nullptr);
+  sg.finish();
+  return 0;
+  MPC_CATCH
+}
+
+int64_t mpc_panel_factor(int k, int method, int64_t n, int64_t jb, int64_t kw, double* re,
+                         double* im, int64_t ld, int64_t ps, int64_t* piv, void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
+  if (n < 0 || jb < 0 || kw < 0 || jb + kw > n) return fail("panel outside the matrix");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({re, im, piv})) return MPC_ERR;
+  int64_t e = extent(k, n, jb + kw, ld, ps);
+  double* dr = sg.map(re, e, true, true);
+  double* di = sg.map(im, e, true, true);
+  int64_t* dp = sg.map(piv, n, true, true);
+  int64_t status = -1;
+  if (kw > 0) {
+    WsHolder w(k, n, st);
+    table_for(k)->panel_rec(method == 3, mpc::View{dr, di, ld, ps}, n, jb, kw, dp, w.ws, st);
+    status = w.read_status();
+  }
+  sg.finish();
+  return status;
+  MPC_CATCH
+}
+
+int mpc_laswp(int k, int64_t ncols, double* re, double* im, int64_t ld, int64_t ps,
+              const int64_t* piv, int64_t r0, int64_t r1, void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (r0 < 0 || r1 < r0 || ncols < 0) return fail("bad interchange range");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({re, im, piv})) return MPC_ERR;
+  // rows touched: up to max(piv[r0..r1)) -- host mode stages the whole
+  // leading r1.. rows range conservatively from the pivots
+  int64_t rows = r1;
+  if (sg.host()) {
+    for (int64_t r = r0; r < r1; r++) rows = std::max(rows, piv[r] + 1);
+  }
+  int64_t e = sg.host() ? extent(k, rows, ncols, ld, ps) : 0;
+  double* dr = sg.map(re, e, true, true);
+  double* di = sg.map(im, e, true, true);
+  const int64_t* dp = sg.map(const_cast<int64_t*>(piv), r1, true, false);
+  table_for(k)->laswp(mpc::View{dr, di, ld, ps}, 0, ncols, dp, r0, r1, st, nullptr);
+  sg.finish();
+  return 0;
+  MPC_CATCH
+}
+
+int64_t mpc_lu_panel(int k, int method, int64_t n, double* re, double* im, int64_t* piv,
+                     int64_t jb, int64_t kw, void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
+  if (n < 0 || jb < 0 || kw < 0 || jb + kw > n) return fail("panel outside the matrix");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({re, im, piv})) return MPC_ERR;
+  int64_t e = extent(k, n, n, n, n * n);
+  double* dr = sg.map(re, e, true, true);
+  double* di = sg.map(im, e, true, true);
+  int64_t* dp = sg.map(piv, n, true, true);
+  int64_t status = -1;
+  if (kw > 0) {
+    WsHolder w(k, n, st);
+    table_for(k)->lu_panel(method == 3, mpc::View{dr, di, n, n * n}, n, jb, kw, dp, w.ws, st);
+    status = w.read_status();
+  }
+  sg.finish();
+  return status;
+  MPC_CATCH
+}
+
+int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* im, int64_t* piv,
+                  void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
+  if (n < 0) return fail("negative dimension");
+  if (n > 0 && (K < 1 || K > n)) return fail("panel width K outside [1, n]");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({re, im, piv})) return MPC_ERR;
+  int64_t e = extent(k, n, n, n, n * n);
+  double* dr = sg.map(re, e, true, true);
+  double* di = sg.map(im, e, true, true);
+  int64_t* dp = sg.map(piv, n, false, true);
+  int64_t status = -1;
+  if (n > 0) {
+    iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dp, n);
+    WsHolder w(k, n, st);
+    table_for(k)->getrf(method == 3, mpc::View{dr, di, n, n * n}, n, K, dp, w.ws, st);
+    status = w.read_status();
+  }
+  sg.finish();
+  return status;
+  MPC_CATCH
+}
+
+int mpc_getrs(int k, int method, int64_t n, const double* re, const double* im,
+              const int64_t* piv, double* b_re, double* b_im, void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
+  if (n < 0) return fail("negative dimension");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(st);
+  if (!sg.classify({re, im, piv, b_re, b_im})) return MPC_ERR;
+  int64_t e = extent(k, n, n, n, n * n);
+  double* dr = sg.map(const_cast<double*>(re), e, true, false);
+  double* di = sg.map(const_cast<double*>(im), e, true, false);
+  const int64_t* dp = sg.map(const_cast<int64_t*>(piv), n, true, false);
+  double* dbr = sg.map(b_re, (int64_t)k * n, true, true);
+  double* dbi = sg.map(b_im, (int64_t)k * n, true, true);
+  if (n > 0)
+    table_for(k)->getrs(method == 3, mpc::View{dr, di, n, n * n}, n, dp, dbr, dbi, st);
+  sg.finish();
+  return 0;
+  MPC_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,409 @@
+// expansion.cuh -- device multi-component (DD/TD/QD) expansion arithmetic.
+//
+// Bit-exact restatement of the reference's numba kernels
+// (/root/reference/pkg/src/mpclu/_kernels.py, cited per function) for sm_100a.
+// Rules that make the GPU bits equal the reference's:
+//   * every FP64 operation is an explicit round-to-nearest intrinsic
+//     (__dadd_rn/__dsub_rn/__dmul_rn), so nvcc can never contract a*b+c into
+//     a DFMA (the reference runs without FMA contraction, _kernels.py:8-9);
+//   * the only DFMA is TwoProd's error term, fma(a,b,-a*b), which equals the
+//     reference's Dekker error term exactly for in-range operands;
+//   * the k>=3 renormalization keeps the reference's data-dependent control
+//     flow (stable sort by (|v| desc, v desc), VecSum, extraction with early
+//     break, repeat-while-overlapping <= 6) using predication instead of
+//     dynamic indexing so everything stays in registers.
+// Comparisons that only steer control flow are done on the integer pipe
+// (bit patterns) to keep the FP64 pipe for arithmetic.
+#pragma once
+#include <cstdint>
+
+namespace mpc {
+
+#define MPC_DI __device__ __forceinline__
+
+MPC_DI double dadd(double a, double b) { return __dadd_rn(a, b); }
+MPC_DI double dsub(double a, double b) { return __dsub_rn(a, b); }
+MPC_DI double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+MPC_DI uint64_t bits(double x) { return (uint64_t)__double_as_longlong(x); }
+MPC_DI uint64_t absbits(double x) { return bits(x) & 0x7FFFFFFFFFFFFFFFull; }
+MPC_DI bool is_nonzero(double x) { return absbits(x) != 0ull; }
+
+// ---------------------------------------------------------------- EFTs
+// _kernels.py:28-34
+MPC_DI void two_sum(double a, double b, double& s, double& e) {
+  double ss = dadd(a, b);
+  double bb = dsub(ss, a);
+  e = dadd(dsub(a, dsub(ss, bb)), dsub(b, bb));
+  s = ss;
+}
+// _kernels.py:37-42
+MPC_DI void quick_two_sum(double a, double b, double& s, double& e) {
+  double ss = dadd(a, b);
+  e = dsub(b, dsub(ss, a));
+  s = ss;
+}
+// _kernels.py:45-60 (Dekker there; FMA form here, bit-identical in range)
+MPC_DI void two_prod(double a, double b, double& p, double& e) {
+  double pp = dmul(a, b);
+  e = __fma_rn(a, b, -pp);
+  p = pp;
+}
+
+// ------------------------------------------------------- DD fast paths
+// _kernels.py:146-155 (accurate add)
+MPC_DI void dd_add(double x0, double x1, double y0, double y1, double& r0, double& r1) {
+  double s1, s2, t1, t2;
+  two_sum(x0, y0, s1, s2);
+  two_sum(x1, y1, t1, t2);
+  s2 = dadd(s2, t1);
+  quick_two_sum(s1, s2, s1, s2);
+  s2 = dadd(s2, t2);
+  quick_two_sum(s1, s2, r0, r1);
+}
+// _kernels.py:158-164
+MPC_DI void dd_mul(double x0, double x1, double y0, double y1, double& r0, double& r1) {
+  double p, e;
+  two_prod(x0, y0, p, e);
+  double t = dadd(dmul(x0, y1), dmul(x1, y0));
+  e = dadd(e, dadd(t, dmul(x1, y1)));
+  quick_two_sum(p, e, r0, r1);
+}
+
+// ------------------------------------------------------------ expansion
+template <int K>
+struct Exp {
+  double c[K];
+};
+
+template <int K>
+MPC_DI Exp<K> exp_zero() {
+  Exp<K> r;
+#pragma unroll
+  for (int i = 0; i < K; i++) r.c[i] = 0.0;
+  return r;
+}
+
+template <int K>
+MPC_DI Exp<K> exp_neg(const Exp<K>& x) {
+  Exp<K> r;
+#pragma unroll
+  for (int i = 0; i < K; i++) r.c[i] = -x.c[i];
+  return r;
+}
+
+// exp_abs_core, _kernels.py:258-265
+template <int K>
+MPC_DI Exp<K> exp_abs(const Exp<K>& x) {
+  return (x.c[0] < 0.0) ? exp_neg(x) : x;
+}
+
+// sort key for (|v| desc, v desc): equal keys <=> the reference's insertion
+// sort would not move one past the other (+0 and -0 compare equal there).
+MPC_DI uint64_t sort_key(double v) {
+  uint64_t a = absbits(v);
+  uint64_t pos = (a != 0ull && !(bits(v) >> 63)) ? 1ull : 0ull;
+  return (a << 1) | pos;
+}
+
+// _sort_desc, _kernels.py:67-78.  Insertion sort written as the equivalent
+// bubble network of strict compare-exchanges (stable, same permutation),
+// restricted to the first m entries (m <= M, runtime).
+template <int M>
+MPC_DI void sort_desc(double (&buf)[M], int m) {
+  uint64_t key[M];
+#pragma unroll
+  for (int i = 0; i < M; i++) key[i] = sort_key(buf[i]);
+#pragma unroll
+  for (int i = 1; i < M; i++) {
+#pragma unroll
+    for (int j = i - 1; j >= 0; j--) {
+      bool sw = (i < m) && (key[j] < key[j + 1]);
+      double a = buf[j], b = buf[j + 1];
+      uint64_t ka = key[j], kb = key[j + 1];
+      buf[j] = sw ? b : a;
+      buf[j + 1] = sw ? a : b;
+      key[j] = sw ? kb : ka;
+      key[j + 1] = sw ? ka : kb;
+    }
+  }
+}
+
+// _vecsum_extract, _kernels.py:81-105, on buf[0..m) (m <= M runtime)
+template <int M, int K>
+MPC_DI void vecsum_extract(double (&buf)[M], int m, Exp<K>& out) {
+  double s = 0.0;
+  bool started = false;
+#pragma unroll
+  for (int i = M - 1; i >= 0; i--) {
+    if (i < m) {
+      if (!started) {
+        s = buf[i];
+        started = true;
+      } else {
+        double e;
+        two_sum(buf[i], s, s, e);
+        buf[i + 1 < M ? i + 1 : M - 1] = e;
+      }
+    }
+  }
+  buf[0] = s;
+#pragma unroll
+  for (int i = 0; i < K; i++) out.c[i] = 0.0;
+  int j = 0;
+  double eps = buf[0];
+  bool done = false;
+#pragma unroll
+  for (int i = 0; i < M - 1; i++) {
+    if (!done && i < m - 1) {
+      double r, enew;
+      two_sum(eps, buf[i + 1], r, enew);
+      if (is_nonzero(enew)) {
+        if (j >= K - 1) {
+          eps = r;
+          done = true;
+        } else {
+#pragma unroll
+          for (int q = 0; q < K; q++)
+            if (q == j) out.c[q] = r;
+          j++;
+          eps = enew;
+        }
+      } else {
+        eps = r;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < K; q++)
+    if (q == j) out.c[q] = eps;
+}
+
+// np.spacing(|x|) for the overlap test
+MPC_DI double spacing_abs(double x) {
+  uint64_t a = absbits(x);
+  double ax = __longlong_as_double((long long)a);
+  if (a >= 0x7FF0000000000000ull) return dsub(ax, ax);  // inf/nan -> nan
+  double nx = __longlong_as_double((long long)(a + 1ull));
+  return dsub(nx, ax);
+}
+
+// _is_nonoverlapping, _kernels.py:108-121
+template <int K>
+MPC_DI bool is_nonoverlapping(const Exp<K>& o) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < K - 1; i++) {
+    double hi = o.c[i], lo = o.c[i + 1];
+    if (!is_nonzero(hi)) {
+      if (is_nonzero(lo)) ok = false;
+    } else {
+      double half = dmul(0.5, spacing_abs(hi));
+      if (fabs(lo) > half || dadd(hi, lo) != hi) ok = false;
+    }
+  }
+  return ok;
+}
+
+// renorm, _kernels.py:124-139 on buf[0..m) (buf clobbered)
+template <int M, int K>
+MPC_DI Exp<K> renorm(double (&buf)[M], int m) {
+  Exp<K> out;
+  sort_desc<M>(buf, m);
+  vecsum_extract<M, K>(buf, m, out);
+  int it = 0;
+  while (!is_nonoverlapping<K>(out) && it < 6) {
+    double b2[K];
+#pragma unroll
+    for (int i = 0; i < K; i++) b2[i] = out.c[i];
+    vecsum_extract<K, K>(b2, K, out);
+    it++;
+  }
+  return out;
+}
+
+// exp_add_core, _kernels.py:174-184
+template <int K>
+MPC_DI Exp<K> exp_add(const Exp<K>& x, const Exp<K>& y) {
+  if constexpr (K == 2) {
+    Exp<2> r;
+    dd_add(x.c[0], x.c[1], y.c[0], y.c[1], r.c[0], r.c[1]);
+    return r;
+  } else {
+    double buf[2 * K];
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      buf[i] = x.c[i];
+      buf[K + i] = y.c[i];
+    }
+    return renorm<2 * K, K>(buf, 2 * K);
+  }
+}
+
+// exp_sub_core, _kernels.py:187-197
+template <int K>
+MPC_DI Exp<K> exp_sub(const Exp<K>& x, const Exp<K>& y) {
+  if constexpr (K == 2) {
+    Exp<2> r;
+    dd_add(x.c[0], x.c[1], -y.c[0], -y.c[1], r.c[0], r.c[1]);
+    return r;
+  } else {
+    double buf[2 * K];
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      buf[i] = x.c[i];
+      buf[K + i] = -y.c[i];
+    }
+    return renorm<2 * K, K>(buf, 2 * K);
+  }
+}
+
+// exp_mul_core, _kernels.py:200-222
+template <int K>
+MPC_DI Exp<K> exp_mul(const Exp<K>& x, const Exp<K>& y) {
+  if constexpr (K == 2) {
+    Exp<2> r;
+    dd_mul(x.c[0], x.c[1], y.c[0], y.c[1], r.c[0], r.c[1]);
+    return r;
+  } else {
+    constexpr int M = K * K + K - 1;
+    double buf[M];
+    int m = 0;
+#pragma unroll
+    for (int s = 0; s < K - 1; s++) {
+#pragma unroll
+      for (int i = 0; i < s + 1; i++) {
+        double p, e;
+        two_prod(x.c[i], y.c[s - i], p, e);
+        buf[m] = p;
+        buf[m + 1] = e;
+        m += 2;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; i++) buf[m++] = dmul(x.c[i], y.c[K - 1 - i]);
+#pragma unroll
+    for (int i = 1; i < K; i++) buf[m++] = dmul(x.c[i], y.c[K - i]);
+    return renorm<M, K>(buf, M);
+  }
+}
+
+// exp_div_core, _kernels.py:225-255 (long division, k+1 quotient digits;
+// generic renorm even for k = 2, exactly as the reference)
+template <int K>
+MPC_DI Exp<K> exp_div(const Exp<K>& x, const Exp<K>& y) {
+  double q[K + 1];
+#pragma unroll
+  for (int i = 0; i < K + 1; i++) q[i] = 0.0;
+  Exp<K> r = x;
+  int nq = 0;
+  bool stop = false;
+#pragma unroll
+  for (int it = 0; it < K + 1; it++) {
+    if (!stop) {
+      double qi = __ddiv_rn(r.c[0], y.c[0]);
+#pragma unroll
+      for (int s = 0; s < K + 1; s++)
+        if (s == it) q[s] = qi;
+      nq++;
+      if (!is_nonzero(qi) || it == K) {
+        stop = true;
+      } else {
+        double buf[3 * K];
+#pragma unroll
+        for (int i = 0; i < K; i++) buf[i] = r.c[i];
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+          double p, e;
+          two_prod(qi, y.c[i], p, e);
+          buf[K + 2 * i] = -p;
+          buf[K + 2 * i + 1] = -e;
+        }
+        r = renorm<3 * K, K>(buf, 3 * K);
+      }
+    }
+  }
+  return renorm<K + 1, K>(q, nq);
+}
+
+// ------------------------------------------------------ complex scalars
+template <int K>
+struct Cx {
+  Exp<K> re, im;
+};
+
+// cmul_3m_core, _kernels.py:527-537
+template <int K>
+MPC_DI Cx<K> cmul3(const Exp<K>& ar, const Exp<K>& ai, const Exp<K>& br, const Exp<K>& bi) {
+  Exp<K> s1 = exp_mul(ar, br);
+  Exp<K> s2 = exp_mul(ai, bi);
+  Cx<K> o;
+  o.re = exp_sub(s1, s2);
+  Exp<K> s3 = exp_add(ar, ai);
+  Exp<K> t = exp_add(br, bi);
+  s3 = exp_mul(s3, t);
+  s3 = exp_sub(s3, s1);
+  o.im = exp_sub(s3, s2);
+  return o;
+}
+
+// cmul_3m_core with the two operand sums precomputed (same bits: the sums are
+// the same exp_add calls, hoisted out of the inner loop)
+template <int K>
+MPC_DI Cx<K> cmul3_pre(const Exp<K>& ar, const Exp<K>& ai, const Exp<K>& sa, const Exp<K>& br,
+                       const Exp<K>& bi, const Exp<K>& sb) {
+  Exp<K> s1 = exp_mul(ar, br);
+  Exp<K> s2 = exp_mul(ai, bi);
+  Cx<K> o;
+  o.re = exp_sub(s1, s2);
+  Exp<K> s3 = exp_mul(sa, sb);
+  s3 = exp_sub(s3, s1);
+  o.im = exp_sub(s3, s2);
+  return o;
+}
+
+// cmul_4m_core, _kernels.py:539-546
+template <int K>
+MPC_DI Cx<K> cmul4(const Exp<K>& ar, const Exp<K>& ai, const Exp<K>& br, const Exp<K>& bi) {
+  Exp<K> s1 = exp_mul(ar, br);
+  Exp<K> s2 = exp_mul(ai, bi);
+  Cx<K> o;
+  o.re = exp_sub(s1, s2);
+  s1 = exp_mul(ai, br);
+  s2 = exp_mul(ar, bi);
+  o.im = exp_add(s1, s2);
+  return o;
+}
+
+template <int K>
+MPC_DI Cx<K> cmul(bool use3m, const Exp<K>& ar, const Exp<K>& ai, const Exp<K>& br,
+                  const Exp<K>& bi) {
+  return use3m ? cmul3(ar, ai, br, bi) : cmul4(ar, ai, br, bi);
+}
+
+// cdiv_core, _kernels.py:549-561
+template <int K>
+MPC_DI Cx<K> cdiv(const Exp<K>& ar, const Exp<K>& ai, const Exp<K>& br, const Exp<K>& bi) {
+  Exp<K> s1 = exp_mul(br, br);
+  Exp<K> s2 = exp_mul(bi, bi);
+  s1 = exp_add(s1, s2);  // d
+  s2 = exp_mul(ar, br);
+  Exp<K> s3 = exp_mul(ai, bi);
+  s2 = exp_add(s2, s3);
+  s3 = exp_mul(ai, br);
+  Exp<K> t = exp_mul(ar, bi);
+  s3 = exp_sub(s3, t);
+  Cx<K> o;
+  o.re = exp_div(s2, s1);
+  o.im = exp_div(s3, s1);
+  return o;
+}
+
+// pivot comparator, _pivot_row's test (cand - best)[0] > 0 (_kernels.py:586-587)
+template <int K>
+MPC_DI bool exp_greater(const Exp<K>& a, const Exp<K>& b) {
+  Exp<K> d = exp_sub(a, b);
+  return d.c[0] > 0.0;
+}
+
+}  // namespace mpc

@@ -1,0 +1,867 @@
+// kernels.cuh -- sm_100a kernels and the host-side launch logic for the
+// complex multi-component GEMM and blocked LU (templated on the component
+// count K; instantiated per K in inst_k*.cu).
+//
+// Reference path (paths relative to /root/reference/pkg/src/mpclu/):
+//   cgemm_3m / cgemm_4m   cmatrix.py:145-177   -> gemm_kernel<MODE_G3/G4>
+//   rgemm_naive/blocked   rgemm.py:53-73, _kernels.py:363-434 -> MODE_REAL
+//   mat_add_k             _kernels.py:327-342  -> mat_add_kernel
+//   renorm_planes         _kernels.py:485-499  -> renorm_planes_kernel
+//   lu_panel              _kernels.py:611-665  -> panel_rec (pivot/step kernels + S)
+//   trsm_ll_unit          _kernels.py:668-705  -> trsm_rec (diag kernel + S)
+//   lu._factor            lu.py:129-163        -> getrf
+//   solve_fb              _kernels.py:708-775  -> getrs
+//
+// Bit-exactness contract: every output element keeps the
+// reference's exact sequence of expansion operations.  GEMM chains are
+// output-stationary, t-ascending, never split along the inner dimension; the
+// in-panel / TRSM updates ("S" mode) keep each element's chained subtractions
+// a -= cmul(l, u) in column order; row interchanges are deferred (LASWP),
+// which commutes with the row operations.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <algorithm>
+#include "expansion.cuh"
+#include "prof.h"
+
+namespace mpc {
+
+// ------------------------------------------------------------------ views
+struct View {  // planar complex (or real: im unused) sub-matrix
+  double* re;
+  double* im;
+  int64_t ld;  // row stride (elements)
+  int64_t ps;  // plane (limb) stride (elements)
+  __host__ __device__ View sub(int64_t r, int64_t c) const {
+    return View{re + r * ld + c, im ? im + r * ld + c : nullptr, ld, ps};
+  }
+};
+
+template <int K>
+MPC_DI Exp<K> ldexp_(const double* p, int64_t ps) {
+  Exp<K> e;
+#pragma unroll
+  for (int c = 0; c < K; c++) e.c[c] = p[c * ps];
+  return e;
+}
+template <int K>
+MPC_DI void stexp_(double* p, int64_t ps, const Exp<K>& e) {
+#pragma unroll
+  for (int c = 0; c < K; c++) p[c * ps] = e.c[c];
+}
+
+// --------------------------------------------------------- GEMM family
+enum Mode { MODE_REAL = 0, MODE_G3 = 1, MODE_G4 = 2, MODE_S3 = 3, MODE_S4 = 4 };
+
+template <int MODE>
+struct ModeInfo;
+// NLOAD operands staged from global per side (re[, im]); NS smem slots per
+// side (3M adds the Re+Im sum slot, formed once per staged element);
+// NACC expansions accumulated per output element.
+template <> struct ModeInfo<MODE_REAL> { static constexpr int NLOAD = 1, NS = 1, NACC = 1; static constexpr bool SUMS = false, CHAINED = false; };
+template <> struct ModeInfo<MODE_G3>   { static constexpr int NLOAD = 2, NS = 3, NACC = 3; static constexpr bool SUMS = true,  CHAINED = false; };
+template <> struct ModeInfo<MODE_G4>   { static constexpr int NLOAD = 2, NS = 2, NACC = 4; static constexpr bool SUMS = false, CHAINED = false; };
+template <> struct ModeInfo<MODE_S3>   { static constexpr int NLOAD = 2, NS = 3, NACC = 2; static constexpr bool SUMS = true,  CHAINED = true; };
+template <> struct ModeInfo<MODE_S4>   { static constexpr int NLOAD = 2, NS = 2, NACC = 2; static constexpr bool SUMS = false, CHAINED = true; };
+
+struct GemmArgs {
+  int64_t m, n, l;  // C (m x l) op= A (m x n) * B (n x l)
+  View a, b, c;
+  int epi;  // G modes: 0 -> C = P, 1 -> C = C - P (lu.py:157-161 order)
+  const int64_t* status;  // LU early-out: skip when *status >= 0
+};
+
+MPC_DI void cp_async8(void* smem_ptr, const double* gptr, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gptr), "r"(sz));
+}
+MPC_DI void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+MPC_DI void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// One CTA computes a BM x BN tile of C with (BM/TM) x (BN/TN) threads; each
+// thread owns a TM x TN strided micro-tile and NACC expansion chains per
+// element.  Inner dimension staged through shared memory in BK slabs with a
+// two-stage cp.async pipeline.  Smem layout per stage:
+//   As[NS][K][BM][BK], Bs[NS][K][BK][BN]   (limb planes kept separate)
+template <int K, int MODE, int BM, int BN, int BK, int TM, int TN>
+struct GemmCfg {
+  using MI = ModeInfo<MODE>;
+  static constexpr int SX = BN / TN, SY = BM / TM, NT = SX * SY;
+  static constexpr int A_STAGE = MI::NS * K * BM * BK;
+  static constexpr int B_STAGE = MI::NS * K * BK * BN;
+  static constexpr size_t SMEM = sizeof(double) * 2 * (A_STAGE + B_STAGE);
+};
+
+template <int K, int MODE, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT)
+    gemm_kernel(GemmArgs g) {
+  using Cfg = GemmCfg<K, MODE, BM, BN, BK, TM, TN>;
+  using MI = ModeInfo<MODE>;
+  constexpr int SX = Cfg::SX, SY = Cfg::SY, NT = Cfg::NT;
+  constexpr int NS = MI::NS, NL = MI::NLOAD, NACC = MI::NACC;
+  constexpr int A_STAGE = Cfg::A_STAGE, B_STAGE = Cfg::B_STAGE;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + 2 * A_STAGE;
+
+  if (g.status != nullptr && *g.status >= 0) return;
+  const int tid = threadIdx.x;
+  const int tx = tid % SX, ty = tid / SX;
+  const int64_t row0 = (int64_t)blockIdx.y * BM, col0 = (int64_t)blockIdx.x * BN;
+
+  // accumulators
+  Exp<K> acc[TM][TN][NACC];
+#pragma unroll
+  for (int r = 0; r < TM; r++)
+#pragma unroll
+    for (int c = 0; c < TN; c++) {
+      if constexpr (MI::CHAINED) {
+        int64_t gi = row0 + ty + r * SY, gj = col0 + tx + c * SX;
+        if (gi < g.m && gj < g.l) {
+          acc[r][c][0] = ldexp_<K>(g.c.re + gi * g.c.ld + gj, g.c.ps);
+          acc[r][c][1] = ldexp_<K>(g.c.im + gi * g.c.ld + gj, g.c.ps);
+        } else {
+          acc[r][c][0] = exp_zero<K>();
+          acc[r][c][1] = exp_zero<K>();
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NACC; q++) acc[r][c][q] = exp_zero<K>();
+      }
+    }
+
+  auto load_stage = [&](int st, int64_t t0) {
+    double* as = As + st * A_STAGE;
+    double* bs = Bs + st * B_STAGE;
+    constexpr int AE = NL * K * BM * BK;
+    for (int e = tid; e < AE; e += NT) {
+      int tt = e % BK;
+      int r = (e / BK) % BM;
+      int c = (e / (BK * BM)) % K;
+      int op = e / (BK * BM * K);
+      int64_t gi = row0 + r, gt = t0 + tt;
+      bool v = gi < g.m && gt < g.n;
+      const double* base = (op == 0) ? g.a.re : g.a.im;
+      const double* src = v ? base + c * g.a.ps + gi * g.a.ld + gt : base;
+      cp_async8(as + ((op * K + c) * BM + r) * BK + tt, src, v);
+    }
+    constexpr int BE = NL * K * BK * BN;
+    for (int e = tid; e < BE; e += NT) {
+      int cc = e % BN;
+      int tt = (e / BN) % BK;
+      int c = (e / (BN * BK)) % K;
+      int op = e / (BN * BK * K);
+      int64_t gt = t0 + tt, gj = col0 + cc;
+      bool v = gt < g.n && gj < g.l;
+      const double* base = (op == 0) ? g.b.re : g.b.im;
+      const double* src = v ? base + c * g.b.ps + gt * g.b.ld + gj : base;
+      cp_async8(bs + ((op * K + c) * BK + tt) * BN + cc, src, v);
+    }
+  };
+
+  const int64_t nk = (g.n + BK - 1) / BK;
+  if (nk > 0) load_stage(0, 0);
+  cp_async_commit();
+  for (int64_t kt = 0; kt < nk; kt++) {
+    const int st = (int)(kt & 1);
+    if (kt + 1 < nk) {
+      load_stage(st ^ 1, (kt + 1) * BK);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    double* as = As + st * A_STAGE;
+    double* bs = Bs + st * B_STAGE;
+    if constexpr (MI::SUMS) {
+      // slot 2 = Re + Im (mat_add_k / cmul_3m_core's exp_add), once per element
+      for (int e = tid; e < BM * BK; e += NT) {
+        Exp<K> x = ldexp_<K>(as + e, BM * BK);
+        Exp<K> y = ldexp_<K>(as + K * BM * BK + e, BM * BK);
+        stexp_<K>(as + 2 * K * BM * BK + e, BM * BK, exp_add(x, y));
+      }
+      for (int e = tid; e < BK * BN; e += NT) {
+        Exp<K> x = ldexp_<K>(bs + e, BK * BN);
+        Exp<K> y = ldexp_<K>(bs + K * BK * BN + e, BK * BN);
+        stexp_<K>(bs + 2 * K * BK * BN + e, BK * BN, exp_add(x, y));
+      }
+      __syncthreads();
+    }
+    const int tlen = (int)min((int64_t)BK, g.n - kt * BK);
+#pragma unroll
+    for (int t = 0; t < BK; t++) {
+      if (t < tlen) {
+        Exp<K> av[NS][TM], bv[NS][TN];
+#pragma unroll
+        for (int s = 0; s < NS; s++) {
+#pragma unroll
+          for (int r = 0; r < TM; r++)
+            av[s][r] = ldexp_<K>(as + (s * K * BM + ty + r * SY) * BK + t, BM * BK);
+#pragma unroll
+          for (int c = 0; c < TN; c++)
+            bv[s][c] = ldexp_<K>(bs + (s * K * BK + t) * BN + tx + c * SX, BK * BN);
+        }
+#pragma unroll
+        for (int r = 0; r < TM; r++)
+#pragma unroll
+          for (int c = 0; c < TN; c++) {
+            if constexpr (MODE == MODE_REAL) {
+              acc[r][c][0] = exp_add(acc[r][c][0], exp_mul(av[0][r], bv[0][c]));
+            } else if constexpr (MODE == MODE_G3) {
+#pragma unroll
+              for (int q = 0; q < 3; q++)
+                acc[r][c][q] = exp_add(acc[r][c][q], exp_mul(av[q][r], bv[q][c]));
+            } else if constexpr (MODE == MODE_G4) {
+              acc[r][c][0] = exp_add(acc[r][c][0], exp_mul(av[0][r], bv[0][c]));  // rr
+              acc[r][c][1] = exp_add(acc[r][c][1], exp_mul(av[1][r], bv[1][c]));  // ii
+              acc[r][c][2] = exp_add(acc[r][c][2], exp_mul(av[1][r], bv[0][c]));  // ir
+              acc[r][c][3] = exp_add(acc[r][c][3], exp_mul(av[0][r], bv[1][c]));  // ri
+            } else if constexpr (MODE == MODE_S3) {
+              Cx<K> p = cmul3_pre(av[0][r], av[1][r], av[2][r], bv[0][c], bv[1][c], bv[2][c]);
+              acc[r][c][0] = exp_sub(acc[r][c][0], p.re);
+              acc[r][c][1] = exp_sub(acc[r][c][1], p.im);
+            } else {  // MODE_S4
+              Cx<K> p = cmul4(av[0][r], av[1][r], bv[0][c], bv[1][c]);
+              acc[r][c][0] = exp_sub(acc[r][c][0], p.re);
+              acc[r][c][1] = exp_sub(acc[r][c][1], p.im);
+            }
+          }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  // epilogue
+#pragma unroll
+  for (int r = 0; r < TM; r++)
+#pragma unroll
+    for (int c = 0; c < TN; c++) {
+      int64_t gi = row0 + ty + r * SY, gj = col0 + tx + c * SX;
+      if (gi >= g.m || gj >= g.l) continue;
+      int64_t off = gi * g.c.ld + gj;
+      if constexpr (MODE == MODE_REAL) {
+        stexp_<K>(g.c.re + off, g.c.ps, acc[r][c][0]);
+      } else if constexpr (MI::CHAINED) {
+        stexp_<K>(g.c.re + off, g.c.ps, acc[r][c][0]);
+        stexp_<K>(g.c.im + off, g.c.ps, acc[r][c][1]);
+      } else {
+        Exp<K> re, im;
+        if constexpr (MODE == MODE_G3) {  // cmatrix.py:166-168
+          re = exp_sub(acc[r][c][0], acc[r][c][1]);
+          im = exp_sub(exp_sub(acc[r][c][2], acc[r][c][0]), acc[r][c][1]);
+        } else {  // cmatrix.py:153
+          re = exp_sub(acc[r][c][0], acc[r][c][1]);
+          im = exp_add(acc[r][c][2], acc[r][c][3]);
+        }
+        if (g.epi == 1) {  // lu.py:158-161: A22 := mat_sub(A22, P)
+          re = exp_sub(ldexp_<K>(g.c.re + off, g.c.ps), re);
+          im = exp_sub(ldexp_<K>(g.c.im + off, g.c.ps), im);
+        }
+        stexp_<K>(g.c.re + off, g.c.ps, re);
+        stexp_<K>(g.c.im + off, g.c.ps, im);
+      }
+    }
+}
+
+// ------------------------------------------------------- elementwise
+// mat_add_k, _kernels.py:327-342: C = A + sign*B (sign = +-1)
+template <int K>
+__global__ void mat_add_kernel(int64_t rows, int64_t cols, View a, View b, View c, double sign) {
+  int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols, j = e % cols;
+    Exp<K> x = ldexp_<K>(a.re + i * a.ld + j, a.ps);
+    Exp<K> y = ldexp_<K>(b.re + i * b.ld + j, b.ps);
+#pragma unroll
+    for (int q = 0; q < K; q++) y.c[q] = dmul(sign, y.c[q]);
+    stexp_<K>(c.re + i * c.ld + j, c.ps, exp_add(x, y));
+  }
+}
+
+// renorm_planes, _kernels.py:485-499 (in place)
+template <int K>
+__global__ void renorm_planes_kernel(int64_t rows, int64_t cols, View a) {
+  int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols, j = e % cols;
+    double buf[K];
+#pragma unroll
+    for (int q = 0; q < K; q++) buf[q] = a.re[q * a.ps + i * a.ld + j];
+    Exp<K> o = renorm<K, K>(buf, K);
+    stexp_<K>(a.re + i * a.ld + j, a.ps, o);
+  }
+}
+
+// ------------------------------------------------------------ pivoting
+// Pivot candidate: (|Re| + |Im|, row), _pivot_row (_kernels.py:568-594).
+// Reduction order-independence: the reference keeps the FIRST row whose
+// value is strictly greater (sign of the exact expansion difference), i.e.
+// the lowest row among the maxima; `better` is that total preorder with
+// ties to the lower row, so any reduction tree returns the same row.
+template <int K>
+struct Cand {
+  Exp<K> v;
+  int64_t row;  // -1: no nonzero candidate
+};
+
+template <int K>
+MPC_DI bool cand_better(const Cand<K>& a, const Cand<K>& b) {
+  if (a.row < 0) return false;
+  if (b.row < 0) return true;
+  Exp<K> d = exp_sub(a.v, b.v);
+  if (d.c[0] > 0.0) return true;
+  if (d.c[0] < 0.0) return false;
+  return a.row < b.row;
+}
+
+template <int K>
+MPC_DI Cand<K> make_cand(const View& A, int64_t i, int64_t j) {
+  Exp<K> t = exp_abs(ldexp_<K>(A.re + i * A.ld + j, A.ps));
+  Exp<K> u = exp_abs(ldexp_<K>(A.im + i * A.ld + j, A.ps));
+  Cand<K> c;
+  c.v = exp_add(t, u);
+  // the reference only accepts cand when (cand - best)[0] > 0, best starting at 0
+  c.row = exp_greater(c.v, exp_zero<K>()) ? i : -1;
+  return c;
+}
+
+template <int K>
+MPC_DI Cand<K> shfl_cand(const Cand<K>& c, int off) {
+  Cand<K> o;
+#pragma unroll
+  for (int q = 0; q < K; q++) o.v.c[q] = __shfl_down_sync(0xffffffffu, c.v.c[q], off);
+  o.row = __shfl_down_sync(0xffffffffu, c.row, off);
+  return o;
+}
+
+// block-wide argmax; result valid in thread 0
+template <int K, int NT>
+MPC_DI Cand<K> block_reduce_cand(Cand<K> c) {
+  __shared__ Exp<K> sv[NT / 32];
+  __shared__ int64_t sr[NT / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Cand<K> o = shfl_cand(c, off);
+    if (cand_better(o, c)) c = o;
+  }
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sv[w] = c.v;
+    sr[w] = c.row;
+  }
+  __syncthreads();
+  if (w == 0) {
+    if (lane < NT / 32) {
+      c.v = sv[lane];
+      c.row = sr[lane];
+    } else {
+      c.row = -1;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      Cand<K> o = shfl_cand(c, off);
+      if (cand_better(o, c)) c = o;
+    }
+  }
+  return c;
+}
+
+struct PanelWs {     // device workspace for the pivot reductions
+  double* pv;        // [maxblocks][K]
+  int64_t* prow;     // [maxblocks]
+  unsigned* counter; // last-block detection
+  int64_t* status;   // -1 ok, else first singular column
+};
+
+constexpr int PNT = 256;  // threads per block of the panel kernels
+
+// Final stage shared by the pivot kernels: the last block to finish reduces
+// the per-block partials (in block order), records piv[j] and swaps rows j
+// and p inside the active column range [c0, cend) (the other columns are
+// swapped later by LASWP, which commutes with the row operations).
+template <int K>
+MPC_DI void pivot_finish(const View& A, int64_t j, int64_t c0, int64_t cend, int64_t* piv,
+                         PanelWs ws, Cand<K> mine) {
+  __shared__ bool last;
+  __shared__ int64_t prow_s;
+  __threadfence();  // every thread's row updates visible before the arrival count
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    stexp_<K>(ws.pv + blockIdx.x * K, 1, mine.v);
+    ws.prow[blockIdx.x] = mine.row;
+    __threadfence();
+    unsigned done = atomicAdd(ws.counter, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  Cand<K> c;
+  c.row = -1;
+  c.v = exp_zero<K>();
+  for (int64_t b = threadIdx.x; b < gridDim.x; b += PNT) {
+    Cand<K> o;
+#pragma unroll
+    for (int q = 0; q < K; q++) o.v.c[q] = __ldcg(ws.pv + b * K + q);
+    o.row = __ldcg(ws.prow + b);
+    if (cand_better(o, c)) c = o;
+  }
+  c = block_reduce_cand<K, PNT>(c);
+  if (threadIdx.x == 0) {
+    prow_s = c.row;
+    *ws.counter = 0u;
+    if (c.row < 0) {
+      if (*ws.status < 0) *ws.status = j;  // lu_panel returns j (_kernels.py:622-624)
+    } else {
+      piv[j] = c.row;
+    }
+  }
+  __syncthreads();
+  int64_t p = prow_s;
+  if (p < 0 || p == j) return;
+  int64_t w = cend - c0;
+  for (int64_t e = threadIdx.x; e < 2 * K * w; e += PNT) {
+    int64_t t = c0 + e % w;
+    int q = (int)(e / w);
+    double* base = (q < K) ? A.re + q * A.ps : A.im + (q - K) * A.ps;
+    double x = __ldcg(base + j * A.ld + t);
+    double y = __ldcg(base + p * A.ld + t);
+    base[j * A.ld + t] = y;
+    base[p * A.ld + t] = x;
+  }
+}
+
+// pivot search for the first column j of a base panel
+template <int K>
+__global__ void __launch_bounds__(PNT) pivot_first_kernel(View A, int64_t n, int64_t j,
+                                                           int64_t c0, int64_t cend,
+                                                           int64_t* piv, PanelWs ws) {
+  if (*ws.status >= 0) return;
+  int64_t i = j + (int64_t)blockIdx.x * PNT + threadIdx.x;
+  Cand<K> c;
+  c.row = -1;
+  c.v = exp_zero<K>();
+  if (i < n) c = make_cand<K>(A, i, j);
+  c = block_reduce_cand<K, PNT>(c);
+  pivot_finish<K>(A, j, c0, cend, piv, ws, c);
+}
+
+// Column step j of lu_panel (_kernels.py:627-664) restricted to the base
+// panel's columns (j, cend), fused with the pivot search of column j+1.
+// One thread per row i > j: l = cdiv(a_ij, a_jj); a_ij = l;
+// a_it -= cmul(l, a_jt) for t in (j, cend).
+template <int K>
+__global__ void __launch_bounds__(PNT) panel_step_kernel(View A, int64_t n, int64_t j,
+                                                          int64_t c0, int64_t cend, int use3m,
+                                                          int64_t* piv, PanelWs ws) {
+  if (*ws.status >= 0) return;
+  int64_t i = j + 1 + (int64_t)blockIdx.x * PNT + threadIdx.x;
+  Cand<K> c;
+  c.row = -1;
+  c.v = exp_zero<K>();
+  if (i < n) {
+    Exp<K> ar = ldexp_<K>(A.re + i * A.ld + j, A.ps);
+    Exp<K> ai = ldexp_<K>(A.im + i * A.ld + j, A.ps);
+    Exp<K> br = ldexp_<K>(A.re + j * A.ld + j, A.ps);
+    Exp<K> bi = ldexp_<K>(A.im + j * A.ld + j, A.ps);
+    Cx<K> l = cdiv(ar, ai, br, bi);
+    stexp_<K>(A.re + i * A.ld + j, A.ps, l.re);
+    stexp_<K>(A.im + i * A.ld + j, A.ps, l.im);
+    for (int64_t t = j + 1; t < cend; t++) {
+      Exp<K> ur = ldexp_<K>(A.re + j * A.ld + t, A.ps);
+      Exp<K> ui = ldexp_<K>(A.im + j * A.ld + t, A.ps);
+      Cx<K> p = cmul(use3m != 0, l.re, l.im, ur, ui);
+      Exp<K> xr = ldexp_<K>(A.re + i * A.ld + t, A.ps);
+      Exp<K> xi = ldexp_<K>(A.im + i * A.ld + t, A.ps);
+      stexp_<K>(A.re + i * A.ld + t, A.ps, exp_sub(xr, p.re));
+      stexp_<K>(A.im + i * A.ld + t, A.ps, exp_sub(xi, p.im));
+    }
+    if (j + 1 < cend) c = make_cand<K>(A, i, j + 1);
+  }
+  if (j + 1 >= cend) return;  // uniform across the grid
+  c = block_reduce_cand<K, PNT>(c);
+  pivot_finish<K>(A, j + 1, c0, cend, piv, ws, c);
+}
+
+// ---------------------------------------------------------------- LASWP
+// Apply the interchanges piv[r0..r1) in order to columns [col0, col0+ncols)
+// of every limb plane (the deferred part of _swap_rows, _kernels.py:597-608).
+template <int K>
+__global__ void laswp_kernel(View A, int64_t col0, int64_t ncols, const int64_t* piv,
+                             int64_t r0, int64_t r1, const int64_t* status) {
+  int64_t cidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cidx >= ncols) return;
+  int q = blockIdx.y;
+  double* base = (q < K) ? A.re + q * A.ps : A.im + (q - K) * A.ps;
+  int64_t col = col0 + cidx;
+  int64_t rend = r1;
+  if (status != nullptr && *status >= 0 && *status < rend) rend = *status;
+  for (int64_t r = r0; r < rend; r++) {
+    int64_t p = piv[r];
+    if (p != r) {
+      double x = base[r * A.ld + col];
+      base[r * A.ld + col] = base[p * A.ld + col];
+      base[p * A.ld + col] = x;
+    }
+  }
+}
+
+// -------------------------------------------------------------- TRSM
+// Diagonal block of trsm_ll_unit (_kernels.py:687-705): one thread per
+// column, rows r ascending, subtractions s ascending.
+template <int K>
+__global__ void trsm_diag_kernel(View L, View X, int64_t kb, int64_t M, int use3m,
+                                 const int64_t* status) {
+  if (status != nullptr && *status >= 0) return;
+  int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= M) return;
+  for (int64_t r = 1; r < kb; r++) {
+    Exp<K> xr = ldexp_<K>(X.re + r * X.ld + col, X.ps);
+    Exp<K> xi = ldexp_<K>(X.im + r * X.ld + col, X.ps);
+    for (int64_t s = 0; s < r; s++) {
+      Exp<K> lr = ldexp_<K>(L.re + r * L.ld + s, L.ps);
+      Exp<K> li = ldexp_<K>(L.im + r * L.ld + s, L.ps);
+      Exp<K> yr = ldexp_<K>(X.re + s * X.ld + col, X.ps);
+      Exp<K> yi = ldexp_<K>(X.im + s * X.ld + col, X.ps);
+      Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+      xr = exp_sub(xr, p.re);
+      xi = exp_sub(xi, p.im);
+    }
+    stexp_<K>(X.re + r * X.ld + col, X.ps, xr);
+    stexp_<K>(X.im + r * X.ld + col, X.ps, xi);
+  }
+}
+
+// -------------------------------------------------------------- solve
+// solve_fb's interchanges (_kernels.py:711-721): one thread per limb plane
+template <int K>
+__global__ void vec_swap_kernel(double* br, double* bi, int64_t n, const int64_t* piv) {
+  int q = threadIdx.x;
+  if (q >= 2 * K) return;
+  double* b = (q < K) ? br + q * n : bi + (q - K) * n;
+  for (int64_t i = 0; i < n; i++) {
+    int64_t p = piv[i];
+    if (p != i) {
+      double x = b[i];
+      b[i] = b[p];
+      b[p] = x;
+    }
+  }
+}
+
+// Forward substitution, block-diagonal part: rows [r0, r0+kb) in order,
+// x_i -= cmul(L_ij, x_j), j ascending (_kernels.py:734-752).  Single thread.
+template <int K>
+__global__ void fwd_diag_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
+                                int64_t kb, int use3m) {
+  for (int64_t i = r0 + 1; i < r0 + kb; i++) {
+    Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
+    for (int64_t j = r0; j < i; j++) {
+      Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
+      Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
+      Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+      xr = exp_sub(xr, p.re);
+      xi = exp_sub(xi, p.im);
+    }
+    stexp_<K>(br + i, n, xr);
+    stexp_<K>(bi + i, n, xi);
+  }
+}
+
+// Forward substitution, off-diagonal part: rows i >= r0+kb subtract the
+// block's contributions j in [r0, r0+kb) ascending (same per-element order
+// as the reference's row-oriented loop).
+template <int K>
+__global__ void fwd_update_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
+                                  int64_t kb, int use3m) {
+  int64_t i = r0 + kb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
+  for (int64_t j = r0; j < r0 + kb; j++) {
+    Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
+    Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
+    Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+    xr = exp_sub(xr, p.re);
+    xi = exp_sub(xi, p.im);
+  }
+  stexp_<K>(br + i, n, xr);
+  stexp_<K>(bi + i, n, xi);
+}
+
+// Backward substitution, block-diagonal part (rows descending) with the
+// cdiv by U_ii (_kernels.py:753-775).  The blocked order of the
+// off-diagonal subtractions differs from the reference's j-ascending chain,
+// so the solve is tolerance-parity (documented in DESIGN.md).
+template <int K>
+__global__ void bwd_diag_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
+                                int64_t kb, int use3m) {
+  for (int64_t i = r0 + kb - 1; i >= r0; i--) {
+    Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
+    for (int64_t j = i + 1; j < r0 + kb; j++) {
+      Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
+      Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
+      Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+      xr = exp_sub(xr, p.re);
+      xi = exp_sub(xi, p.im);
+    }
+    Exp<K> ur = ldexp_<K>(F.re + i * F.ld + i, F.ps), ui = ldexp_<K>(F.im + i * F.ld + i, F.ps);
+    Cx<K> q = cdiv(xr, xi, ur, ui);
+    stexp_<K>(br + i, n, q.re);
+    stexp_<K>(bi + i, n, q.im);
+  }
+}
+
+template <int K>
+__global__ void bwd_update_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
+                                  int64_t kb, int use3m) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r0) return;
+  Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
+  for (int64_t j = r0; j < r0 + kb; j++) {
+    Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
+    Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
+    Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+    xr = exp_sub(xr, p.re);
+    xi = exp_sub(xi, p.im);
+  }
+  stexp_<K>(br + i, n, xr);
+  stexp_<K>(bi + i, n, xi);
+}
+
+// ===================================================== host-side launchers
+// Algorithmic FP64 operation model v1: DADD,
+// DSUB, DMUL, DFMA each count 1.  The k >= 3 figures count VecSum +
+// extraction of every renorm and exclude sorting / repeat passes.
+template <int K>
+struct OpModel {
+  static constexpr double real_mac = K == 2 ? 31.0 : (K == 3 ? 195.0 : 325.0);
+  // panel / TRSM element update a -= cmul(l, u): cmul + 2 subtractions
+  static constexpr double upd3 = K == 2 ? 173.0 : (K == 3 ? 833.0 : 1323.0);
+  static constexpr double upd4 = K == 2 ? 124.0 : (K == 3 ? 780.0 : 1300.0);
+  static double upd(bool use3m) { return use3m ? upd3 : upd4; }
+};
+
+struct LaunchError {
+  const char* what;
+};
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw LaunchError{what};
+}
+
+inline unsigned cdiv_u(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+template <int K>
+struct Ops {
+  // tile configurations (tuned per K)
+  static constexpr int BM = (K == 2) ? 32 : 16;
+  static constexpr int BN = (K == 2) ? 32 : 16;
+  static constexpr int BK = 8;
+  static constexpr int TM = (K == 2) ? 2 : 1;
+  static constexpr int TN = (K == 2) ? 2 : 1;
+
+  template <int MODE>
+  static void gemm_launch(const GemmArgs& g, cudaStream_t st, int MI_CLASS, double per_elem) {
+    if (g.m <= 0 || g.l <= 0) return;
+    double ops = (double)g.m * (double)g.l * (double)g.n * per_elem;
+    using Cfg = GemmCfg<K, MODE, BM, BN, BK, TM, TN>;
+    auto kern = gemm_kernel<K, MODE, BM, BN, BK, TM, TN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+      attr_set = true;
+    }
+    dim3 grid(cdiv_u(g.l, BN), cdiv_u(g.m, BM));
+    int tok_ = prof_begin(MI_CLASS, ops, st);
+    kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(g);
+    prof_end(tok_, st);
+    check_launch("gemm_kernel");
+  }
+
+  static void rgemm(int64_t m, int64_t n, int64_t l, View a, View b, View c, cudaStream_t st) {
+    GemmArgs g{m, n, l, a, b, c, 0, nullptr};
+    gemm_launch<MODE_REAL>(g, st, PC_GEMM, OpModel<K>::real_mac);
+  }
+
+  // P = A B (epi 0) or C = C - A B (epi 1), 3M or 4M
+  static void cgemm(bool use3m, int64_t m, int64_t n, int64_t l, View a, View b, View c, int epi,
+                    cudaStream_t st, const int64_t* status) {
+    GemmArgs g{m, n, l, a, b, c, epi, status};
+    if (use3m)
+      gemm_launch<MODE_G3>(g, st, PC_GEMM, 3 * OpModel<K>::real_mac);
+    else
+      gemm_launch<MODE_G4>(g, st, PC_GEMM, 4 * OpModel<K>::real_mac);
+  }
+
+  // chained update C -= L (x) U, each element's subtractions in column order
+  static void supdate(bool use3m, int64_t m, int64_t kb, int64_t l, View L, View U, View C,
+                      cudaStream_t st, const int64_t* status) {
+    if (m <= 0 || l <= 0 || kb <= 0) return;
+    GemmArgs g{m, kb, l, L, U, C, 0, status};
+    if (use3m)
+      gemm_launch<MODE_S3>(g, st, PC_SUPD, OpModel<K>::upd3);
+    else
+      gemm_launch<MODE_S4>(g, st, PC_SUPD, OpModel<K>::upd4);
+  }
+
+  static void mat_add(int64_t rows, int64_t cols, View a, View b, View c, double sign,
+                      cudaStream_t st) {
+    int64_t total = rows * cols;
+    if (total <= 0) return;
+    unsigned blocks = (unsigned)std::min<int64_t>(cdiv_u(total, 256), 148 * 16);
+    int tok_ = prof_begin(PC_OTHER, 0.0, st);
+    mat_add_kernel<K><<<blocks, 256, 0, st>>>(rows, cols, a, b, c, sign);
+    prof_end(tok_, st);
+    check_launch("mat_add_kernel");
+  }
+
+  static void renorm_planes(int64_t rows, int64_t cols, View a, cudaStream_t st) {
+    int64_t total = rows * cols;
+    if (total <= 0) return;
+    unsigned blocks = (unsigned)std::min<int64_t>(cdiv_u(total, 256), 148 * 16);
+    int tok_ = prof_begin(PC_OTHER, 0.0, st);
+    renorm_planes_kernel<K><<<blocks, 256, 0, st>>>(rows, cols, a);
+    prof_end(tok_, st);
+    check_launch("renorm_planes_kernel");
+  }
+
+  static void laswp(View A, int64_t col0, int64_t ncols, const int64_t* piv, int64_t r0,
+                    int64_t r1, cudaStream_t st, const int64_t* status) {
+    if (ncols <= 0 || r1 <= r0) return;
+    dim3 grid(cdiv_u(ncols, 128), 2 * K);
+    int tok_ = prof_begin(PC_LASWP, 0.0, st);
+    laswp_kernel<K><<<grid, 128, 0, st>>>(A, col0, ncols, piv, r0, r1, status);
+    prof_end(tok_, st);
+    check_launch("laswp_kernel");
+  }
+
+  static constexpr int TRSM_BASE = 16;
+  // L (kb x kb, unit lower, strictly-lower part read) and X (kb x M) views
+  static void trsm(bool use3m, int64_t kb, int64_t M, View L, View X, cudaStream_t st,
+                   const int64_t* status) {
+    if (kb <= 1 || M <= 0) return;
+    if (kb <= TRSM_BASE) {
+      int tok_ = prof_begin(PC_TRSM, (double)M * (double)(kb * (kb - 1) / 2) * OpModel<K>::upd(use3m), st);
+      trsm_diag_kernel<K><<<cdiv_u(M, 128), 128, 0, st>>>(L, X, kb, M, use3m ? 1 : 0, status);
+      prof_end(tok_, st);
+      check_launch("trsm_diag_kernel");
+      return;
+    }
+    int64_t h = kb / 2;
+    trsm(use3m, h, M, L, X, st, status);
+    supdate(use3m, kb - h, h, M, L.sub(h, 0), X, X.sub(h, 0), st, status);
+    trsm(use3m, kb - h, M, L.sub(h, h), X.sub(h, 0), st, status);
+  }
+
+  static constexpr int PANEL_BASE = 8;
+  // base panel: columns [c0, c0+w) over rows [c0, n), swaps within [c0, c0+w)
+  static void panel_base(bool use3m, View A, int64_t n, int64_t c0, int64_t w, int64_t* piv,
+                         PanelWs ws, cudaStream_t st) {
+    int64_t cend = c0 + w;
+    int tok_ = prof_begin(PC_PANEL, 0.0, st);
+    pivot_first_kernel<K><<<cdiv_u(n - c0, PNT), PNT, 0, st>>>(A, n, c0, c0, cend, piv, ws);
+    prof_end(tok_, st);
+    check_launch("pivot_first_kernel");
+    for (int64_t j = c0; j < cend; j++) {
+      int64_t rows = n - j - 1;
+      if (rows <= 0) break;
+      int tok_ = prof_begin(PC_PANEL, (double)rows * (double)(cend - j - 1) * OpModel<K>::upd(use3m), st);
+      panel_step_kernel<K><<<cdiv_u(rows, PNT), PNT, 0, st>>>(A, n, j, c0, cend, use3m ? 1 : 0,
+                                                              piv, ws);
+      prof_end(tok_, st);
+      check_launch("panel_step_kernel");
+    }
+  }
+
+  // recursive panel factorization of columns [c0, c0+w); on return every
+  // interchange piv[c0..c0+w) has been applied to columns [c0, c0+w)
+  static void panel_rec(bool use3m, View A, int64_t n, int64_t c0, int64_t w, int64_t* piv,
+                        PanelWs ws, cudaStream_t st) {
+    if (w <= PANEL_BASE) {
+      panel_base(use3m, A, n, c0, w, piv, ws, st);
+      return;
+    }
+    int64_t h = ((w / 2 + PANEL_BASE - 1) / PANEL_BASE) * PANEL_BASE;
+    if (h >= w) h = w / 2;
+    panel_rec(use3m, A, n, c0, h, piv, ws, st);
+    laswp(A, c0 + h, w - h, piv, c0, c0 + h, st, ws.status);
+    trsm(use3m, h, w - h, A.sub(c0, c0), A.sub(c0, c0 + h), st, ws.status);
+    supdate(use3m, n - c0 - h, h, w - h, A.sub(c0 + h, c0), A.sub(c0, c0 + h),
+            A.sub(c0 + h, c0 + h), st, ws.status);
+    panel_rec(use3m, A, n, c0 + h, w - h, piv, ws, st);
+    laswp(A, c0, h, piv, c0 + h, c0 + w, st, ws.status);
+  }
+
+  // lu_panel on an n x n matrix: factor [jb, jb+kw) and apply the
+  // interchanges to every other column (full-row swap semantics)
+  static void lu_panel(bool use3m, View A, int64_t n, int64_t jb, int64_t kw, int64_t* piv,
+                       PanelWs ws, cudaStream_t st) {
+    panel_rec(use3m, A, n, jb, kw, piv, ws, st);
+    laswp(A, 0, jb, piv, jb, jb + kw, st, ws.status);
+    laswp(A, jb + kw, n - jb - kw, piv, jb, jb + kw, st, ws.status);
+  }
+
+  // lu._factor (lu.py:129-163), everything on `st`
+  static void getrf(bool use3m, View A, int64_t n, int64_t Kp, int64_t* piv, PanelWs ws,
+                    cudaStream_t st) {
+    for (int64_t jb = 0; jb < n; jb += Kp) {
+      int64_t kw = std::min(Kp, n - jb);
+      lu_panel(use3m, A, n, jb, kw, piv, ws, st);
+      int64_t end = jb + kw;
+      if (end == n) break;
+      int64_t M = n - end;
+      trsm(use3m, kw, M, A.sub(jb, jb), A.sub(jb, end), st, ws.status);
+      cgemm(use3m, M, kw, M, A.sub(end, jb), A.sub(jb, end), A.sub(end, end), 1, st, ws.status);
+    }
+  }
+
+  static constexpr int SOLVE_BLOCK = 32;
+  // solve_fb (_kernels.py:708-775); b overwritten by x
+  static void getrs(bool use3m, View F, int64_t n, const int64_t* piv, double* br, double* bi,
+                    cudaStream_t st) {
+    int u3 = use3m ? 1 : 0;
+    int tok_ = prof_begin(PC_OTHER, 0.0, st);
+    vec_swap_kernel<K><<<1, 32, 0, st>>>(br, bi, n, piv);
+    prof_end(tok_, st);
+    check_launch("vec_swap_kernel");
+    for (int64_t r0 = 0; r0 < n; r0 += SOLVE_BLOCK) {
+      int64_t kb = std::min<int64_t>(SOLVE_BLOCK, n - r0);
+      int tok_ = prof_begin(PC_OTHER, 0.0, st);
+      fwd_diag_kernel<K><<<1, 1, 0, st>>>(F, br, bi, n, r0, kb, u3);
+      prof_end(tok_, st);
+      check_launch("fwd_diag_kernel");
+      int64_t rest = n - r0 - kb;
+      if (rest > 0) {
+        int tok_ = prof_begin(PC_OTHER, 0.0, st);
+        fwd_update_kernel<K><<<cdiv_u(rest, 128), 128, 0, st>>>(F, br, bi, n, r0, kb, u3);
+        prof_end(tok_, st);
+        check_launch("fwd_update_kernel");
+      }
+    }
+    int64_t nb = (n + SOLVE_BLOCK - 1) / SOLVE_BLOCK;
+    for (int64_t b = nb - 1; b >= 0; b--) {
+      int64_t r0 = b * SOLVE_BLOCK;
+      int64_t kb = std::min<int64_t>(SOLVE_BLOCK, n - r0);
+      int tok_ = prof_begin(PC_OTHER, 0.0, st);
+      bwd_diag_kernel<K><<<1, 1, 0, st>>>(F, br, bi, n, r0, kb, u3);
+      prof_end(tok_, st);
+      check_launch("bwd_diag_kernel");
+      if (r0 > 0) {
+        int tok_ = prof_begin(PC_OTHER, 0.0, st);
+        bwd_update_kernel<K><<<cdiv_u(r0, 128), 128, 0, st>>>(F, br, bi, n, r0, kb, u3);
+        prof_end(tok_, st);
+        check_launch("bwd_update_kernel");
+      }
+    }
+  }
+};
+
+}  // namespace mpc

@@ -1,0 +1,241 @@
+"""Complex LU with partial pivoting -- drop-in for mpclu.lu (lu.py:1-282).
+
+``lu_blocked`` / ``lu_normal`` run the whole factorization on the B200
+(libmpcb200 ``mpc_getrf``): a recursive panel (pivot search by block
+argmax, deferred interchanges, chained "S" updates), a right-looking blocked
+TRSM for U12 and the fused 3M/4M trailing update ``A22 -= L21 U12``.  Pivots
+and packed factors are bit-identical to the reference.  ``solve`` runs
+forward substitution bit-identically and backward substitution with a
+blocked order (tolerance parity).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .cmatrix import KernelChoice, PlanarComplexMatrix, _check_k
+from .rmatrix import RealMatrix, check_threads
+
+
+class SingularMatrixError(ValueError):
+    """lu.py:32-35"""
+
+    def __init__(self, column):
+        super().__init__(f"singular matrix at column {column}")
+        self.column = column
+
+
+class ComplexVector:
+    """Planar complex vector: re and im are (k, n) float64 arrays (lu.py:38-82)."""
+
+    __slots__ = ("re", "im")
+
+    def __init__(self, re, im):
+        re = np.ascontiguousarray(re, dtype=np.float64)
+        im = np.ascontiguousarray(im, dtype=np.float64)
+        if re.shape != im.shape or re.ndim != 2:
+            raise ValueError("re and im must be (k, n) arrays of equal shape")
+        self.re = re
+        self.im = im
+
+    @property
+    def k(self):
+        return self.re.shape[0]
+
+    @property
+    def n(self):
+        return self.re.shape[1]
+
+    @classmethod
+    def zeros(cls, n, k):
+        return cls(np.zeros((k, n)), np.zeros((k, n)))
+
+    def copy(self):
+        return ComplexVector(self.re.copy(), self.im.copy())
+
+    def bitwise_equal(self, other):
+        return bool(np.array_equal(self.re, other.re) and np.array_equal(self.im, other.im))
+
+
+@dataclass
+class LinearSystem:
+    """A x = b over planar complex storage (lu.py:85-96)."""
+
+    A: PlanarComplexMatrix
+    b: ComplexVector
+
+    def __post_init__(self):
+        if self.A.rows != self.A.cols:
+            raise ValueError("coefficient matrix must be square")
+        if self.b.n != self.A.rows or self.b.k != self.A.k:
+            raise ValueError("right-hand side does not match the matrix")
+
+
+@dataclass
+class LUFactors:
+    """Packed unit-lower L / U and pivots (lu.py:99-126)."""
+
+    packed: PlanarComplexMatrix
+    pivots: np.ndarray
+    method: str = "3m"
+
+    @property
+    def n(self):
+        return self.packed.rows
+
+    def lower(self):
+        n, k = self.n, self.packed.k
+        L = PlanarComplexMatrix.identity(n, k)
+        for c in range(k):
+            L.re_plane.data[c] += np.tril(self.packed.re_plane.data[c], -1)
+            L.im_plane.data[c] += np.tril(self.packed.im_plane.data[c], -1)
+        return L
+
+    def upper(self):
+        k = self.packed.k
+        U = PlanarComplexMatrix.zeros(self.n, self.n, k)
+        for c in range(k):
+            U.re_plane.data[c] = np.triu(self.packed.re_plane.data[c])
+            U.im_plane.data[c] = np.triu(self.packed.im_plane.data[c])
+        return U
+
+
+def _factor(A, K, method):
+    """lu._factor (lu.py:129-163) as one device call."""
+    n, k = A.rows, A.k
+    _check_k(k)
+    re = A.re_plane.data.copy()
+    im = A.im_plane.data.copy()
+    piv = np.arange(n, dtype=np.int64)
+    if n:
+        st = _lib.check(_lib.lib().mpc_getrf(k, 3 if method == "3m" else 4, n, K, _lib.ptr(re),
+                                             _lib.ptr(im), _lib.ptr(piv), None), "getrf")
+        if st >= 0:
+            raise SingularMatrixError(int(st))
+    packed = PlanarComplexMatrix(RealMatrix(re), RealMatrix(im))
+    return LUFactors(packed=packed, pivots=piv, method=method)
+
+
+def lu_normal(A, threads=1, method="3m"):
+    """Element-wise right-looking factorization (lu.py:166-170)."""
+    if A.rows != A.cols:
+        raise ValueError("matrix must be square")
+    check_threads(threads)
+    if method not in ("3m", "4m"):
+        raise ValueError(f"unknown method {method!r}")
+    return _factor(A, max(A.rows, 1), method)
+
+
+def lu_blocked(A, K, kc=None, threads=1):
+    """Blocked factorization with trailing updates (lu.py:173-187)."""
+    if A.rows != A.cols:
+        raise ValueError("matrix must be square")
+    if not 1 <= K <= A.rows:
+        raise ValueError(f"panel width K={K} outside [1, {A.rows}]")
+    if kc is None:
+        kc = KernelChoice()
+    kc = kc.validate().with_threads(threads)
+    check_threads(threads)
+    if kc.real_kernel in ("strassen", "ozaki"):
+        raise NotImplementedError(
+            f"real_kernel={kc.real_kernel!r} is not on the B200 path yet (DESIGN.md, next rows)")
+    return _factor(A, K, kc.method)
+
+
+def trsm_unit_lower(L11, A12, method="3m", threads=1):
+    """Solve L11 X = A12, L11 unit lower (lu.py:190-202)."""
+    if L11.rows != L11.cols:
+        raise ValueError("L11 must be square")
+    if A12.rows != L11.rows or A12.k != L11.k:
+        raise ValueError("A12 does not match L11")
+    check_threads(threads)
+    _check_k(L11.k)
+    xre = A12.re_plane.data.copy()
+    xim = A12.im_plane.data.copy()
+    k, K, M = xre.shape
+    if K and M:
+        _lib.check(_lib.lib().mpc_trsm_ll_unit(
+            k, 3 if method == "3m" else 4, K, M, _lib.ptr(L11.re_plane.data),
+            _lib.ptr(L11.im_plane.data), K, K * K, _lib.ptr(xre), _lib.ptr(xim), M, K * M, None),
+            "trsm_ll_unit")
+    return PlanarComplexMatrix(RealMatrix(xre), RealMatrix(xim))
+
+
+def solve(f, b):
+    """x from L U x = P b (lu.py:205-218)."""
+    n = f.n
+    if b.n != n or b.k != f.packed.k:
+        raise ValueError("right-hand side does not match the factors")
+    k = f.packed.k
+    _check_k(k)
+    re = np.ascontiguousarray(f.packed.re_plane.data)
+    im = np.ascontiguousarray(f.packed.im_plane.data)
+    diag_zero = (re[0].diagonal() == 0.0) & (im[0].diagonal() == 0.0)
+    if diag_zero.any():
+        raise SingularMatrixError(int(np.argmax(diag_zero)))
+    x = b.copy()
+    piv = np.ascontiguousarray(f.pivots, dtype=np.int64)
+    if n:
+        _lib.check(_lib.lib().mpc_getrs(k, 3 if f.method == "3m" else 4, n, _lib.ptr(re),
+                                        _lib.ptr(im), _lib.ptr(piv), _lib.ptr(x.re),
+                                        _lib.ptr(x.im), None), "getrs")
+    return x
+
+
+def permuted(A, pivots):
+    """Apply the factorization's row interchanges to a copy of A (lu.py:221-229)."""
+    re = A.re_plane.data.copy()
+    im = A.im_plane.data.copy()
+    for i, p in enumerate(pivots):
+        if p != i:
+            re[:, [i, p], :] = re[:, [p, i], :]
+            im[:, [i, p], :] = im[:, [p, i], :]
+    return PlanarComplexMatrix(RealMatrix(re), RealMatrix(im))
+
+
+def max_rel_err(xhat, x):
+    """max_i |xhat_i - x_i| / |x_i| over complex moduli (lu.py:263-282).
+
+    Returned as a float: the difference is formed limb-wise in binary64
+    (the leading-limb difference is exact for nearby values), which is ample
+    for an error *metric*; the reference carries it as an expansion."""
+    if xhat.n != x.n or xhat.k != x.k:
+        raise ValueError("vectors must share length and component count")
+
+    def diff(a, b):
+        d = np.zeros(a.shape[1])
+        for c in range(a.shape[0] - 1, -1, -1):
+            d += a[c] - b[c]
+        return d
+
+    dr, di = diff(xhat.re, x.re), diff(xhat.im, x.im)
+    xr, xi = x.re.sum(axis=0), x.im.sum(axis=0)
+    den = np.hypot(xr, xi)
+    if np.any(den == 0.0):
+        raise ValueError(f"zero true component at index {int(np.argmax(den == 0.0))}")
+    return float(np.max(np.hypot(dr, di) / den)) if x.n else 0.0
+
+
+def factor_inplace(re, im, K, method="3m", piv=None):
+    """In-place variant of lu_blocked on raw planar buffers (no copies):
+    ``re``/``im`` are (k, n, n) float64 C-contiguous numpy arrays (pinned or
+    pageable host memory, staged by the C-ABI) or CUDA tensors (device
+    memory, factored in place on the current stream).  Returns the pivots;
+    raises SingularMatrixError like lu_blocked."""
+    k, n, _ = re.shape
+    _check_k(k)
+    if not 1 <= K <= max(n, 1):
+        raise ValueError(f"panel width K={K} outside [1, {n}]")
+    if piv is None:
+        piv = np.empty(n, dtype=np.int64)
+    stream = None
+    if not isinstance(re, np.ndarray):
+        import torch
+
+        stream = torch.cuda.current_stream(re.device).cuda_stream
+    st = _lib.check(_lib.lib().mpc_getrf(k, 3 if method == "3m" else 4, n, K, _lib.ptr(re),
+                                         _lib.ptr(im), _lib.ptr(piv), stream), "getrf")
+    if st >= 0:
+        raise SingularMatrixError(int(st))
+    return piv

@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's
+golden vectors and the CPU oracle.  Bitwise for GEMM / elementwise / panel /
+TRSM / blocked LU (pivots + packed factors); tolerance for the solve
+(backward substitution is reordered)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD
+
+pytestmark = pytest.mark.gpu
+
+import paper_2403_16013_b200 as mp  # noqa: E402
+from paper_2403_16013_b200 import problems  # noqa: E402
+from paper_2403_16013_b200.digest import digest  # noqa: E402
+from paper_2403_16013_b200.expansion import U_PREC  # noqa: E402
+
+
+def beq(a, b):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+def pc(re, im):
+    return mp.PlanarComplexMatrix(mp.RealMatrix(re), mp.RealMatrix(im))
+
+
+def first_diff(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape:
+        return f"shape {a.shape} vs {b.shape}"
+    idx = np.argwhere(a.view(np.int64) != b.view(np.int64))
+    if len(idx) == 0:
+        return "equal"
+    i = tuple(idx[0])
+    return f"{len(idx)} diffs; first at {i}: {a[i]!r} vs {b[i]!r}"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    mp._lib.require_device()
+
+
+# --------------------------------------------------------- golden vectors
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_golden_elementwise(small, k):
+    A, B = mp.RealMatrix(small[f"madd_A_k{k}"]), mp.RealMatrix(small[f"madd_B_k{k}"])
+    assert beq(mp.mat_add(A, B).data, small[f"madd_k{k}"])
+    assert beq(mp.mat_sub(A, B).data, small[f"msub_k{k}"])
+    R = small[f"rnp_in_k{k}"].copy()
+    assert beq(mp.renorm_planes(R), small[f"rnp_out_k{k}"])
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_golden_gemm(small, k):
+    for shp in ("7x5x6", "16x16x16", "33x17x20"):
+        tag = f"k{k}_{shp}"
+        C = mp.rgemm_naive(mp.RealMatrix(small[f"rg_A_{tag}"]), mp.RealMatrix(small[f"rg_B_{tag}"]))
+        assert beq(C.data, small[f"rg_C_{tag}"]), (tag, first_diff(C.data, small[f"rg_C_{tag}"]))
+        A = pc(small[f"cg_Ar_{tag}"], small[f"cg_Ai_{tag}"])
+        B = pc(small[f"cg_Br_{tag}"], small[f"cg_Bi_{tag}"])
+        for meth in ("3m", "4m"):
+            C = mp.cgemm(A, B, mp.KernelChoice(method=meth))
+            got = np.array([C.re_plane.data, C.im_plane.data])
+            assert beq(got, small[f"cg_{meth}_{tag}"]), (meth, tag,
+                                                          first_diff(got, small[f"cg_{meth}_{tag}"]))
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_golden_lu(small, k):
+    for n in (24, 37):
+        tag = f"k{k}_n{n}"
+        A = pc(small[f"lu_re_{tag}"], small[f"lu_im_{tag}"])
+        for meth in ("3m", "4m"):
+            for Kp in (n, 8, 5):
+                key = f"lu_{meth}_K{Kp if Kp != n else 'n'}_{tag}"
+                if Kp == n:
+                    f = mp.lu_normal(A, method=meth)
+                else:
+                    f = mp.lu_blocked(A, Kp, kc=mp.KernelChoice(method=meth))
+                assert np.array_equal(f.pivots, small[key + "_piv"]), key
+                got = np.array([f.packed.re_plane.data, f.packed.im_plane.data])
+                assert beq(got, small[key]), (key, first_diff(got, small[key]))
+                b = small[key + "_b"]
+                x = mp.solve(f, mp.ComplexVector(b[0], b[1]))
+                xref = small[key + "_x"]
+                err = mp.max_rel_err(x, mp.ComplexVector(xref[0], xref[1]))
+                assert err <= 10 * n * U_PREC[k] * 1e3, (key, err)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_golden_trsm(small, k):
+    L, A = small[f"trsm_L_k{k}"], small[f"trsm_A_k{k}"]
+    for meth in ("3m", "4m"):
+        X = mp.trsm_unit_lower(pc(L[0], L[1]), pc(A[0], A[1]), method=meth)
+        got = np.array([X.re_plane.data, X.im_plane.data])
+        assert beq(got, small[f"trsm_{meth}_k{k}"]), (meth, first_diff(got, small[f"trsm_{meth}_k{k}"]))
+
+
+def test_golden_singular(small):
+    base = small["sing_dep"]
+    A = pc(mp.RealMatrix.from_float64(base, 2).data, np.zeros((2, 3, 3)))
+    with pytest.raises(mp.SingularMatrixError, match="column 1"):
+        mp.lu_normal(A)
+    with pytest.raises(mp.SingularMatrixError, match="column 0"):
+        mp.lu_normal(mp.PlanarComplexMatrix.zeros(4, 4, 2))
+    with pytest.raises(mp.SingularMatrixError, match="column 0"):
+        mp.lu_blocked(mp.PlanarComplexMatrix.zeros(40, 40, 2), 16)
+
+
+# ------------------------------------------------------- vs the oracle
+
+def rand_pc(rng, m, n, k):
+    return (mp.random_matrix(m, n, k, rng).data - 0.0, mp.random_matrix(m, n, k, rng).data)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_cgemm_ragged_vs_oracle(orc, k):
+    rng = np.random.default_rng(7 + k)
+    shapes = [(1, 1, 1), (70, 45, 66), (33, 1, 17), (5, 130, 3), (64, 64, 64)]
+    if k == 2:
+        shapes += [(129, 257, 95)]
+    for (m, n, l) in shapes:
+        ar, ai = rand_pc(rng, m, n, k)
+        br, bi = rand_pc(rng, n, l, k)
+        for meth in ("3m", "4m"):
+            C = mp.cgemm(pc(ar, ai), pc(br, bi), mp.KernelChoice(method=meth))
+            cr, ci = orc.cgemm(ar, ai, br, bi, meth)
+            assert beq(C.re_plane.data, cr), ((m, n, l), meth, first_diff(C.re_plane.data, cr))
+            assert beq(C.im_plane.data, ci), ((m, n, l), meth, first_diff(C.im_plane.data, ci))
+
+
+def test_cgemm_empty_and_epilogue(orc):
+    """Empty inner dimension, empty outputs, and the fused A22 - P epilogue
+    through the C-ABI against the reference's cgemm + mat_sub composition."""
+    rng = np.random.default_rng(3)
+    k = 2
+    Z = mp.cgemm(mp.PlanarComplexMatrix.zeros(5, 0, k), mp.PlanarComplexMatrix.zeros(0, 4, k),
+                 mp.KernelChoice())
+    zr, zi = orc.cgemm(np.zeros((k, 5, 0)), np.zeros((k, 5, 0)), np.zeros((k, 0, 4)),
+                       np.zeros((k, 0, 4)), "3m")
+    assert beq(Z.re_plane.data, zr) and beq(Z.im_plane.data, zi)
+    assert mp.cgemm(mp.PlanarComplexMatrix.zeros(0, 3, k), mp.PlanarComplexMatrix.zeros(3, 2, k),
+                    mp.KernelChoice()).rows == 0
+    lib = mp._lib.lib()
+    for meth in (3, 4):
+        m, n, l = 37, 19, 41
+        ar, ai = rand_pc(rng, m, n, k)
+        br, bi = rand_pc(rng, n, l, k)
+        cr0, ci0 = rand_pc(rng, m, l, k)
+        cr, ci = cr0.copy(), ci0.copy()
+        P = mp._lib.check(lib.mpc_cgemm(k, meth, m, n, l, ar.ctypes.data, ai.ctypes.data, n, m * n,
+                                        br.ctypes.data, bi.ctypes.data, l, n * l, cr.ctypes.data,
+                                        ci.ctypes.data, l, m * l, 1, None), "cgemm")
+        assert P == 0
+        pr, pi = orc.cgemm(ar, ai, br, bi, "3m" if meth == 3 else "4m")
+        assert beq(cr, orc.mat_sub(cr0, pr)) and beq(ci, orc.mat_sub(ci0, pi))
+
+
+def test_real_only_3m_cancels_and_rotation():
+    """test_cgemm.py:43-61: 3M imaginary plane of real-only inputs cancels to
+    exact zeros; multiplication by i is exact."""
+    rng = np.random.default_rng(11)
+    n, k = 16, 3
+    A = mp.PlanarComplexMatrix(mp.random_matrix(n, n, k, rng), mp.RealMatrix.zeros(n, n, k))
+    B = mp.PlanarComplexMatrix(mp.random_matrix(n, n, k, rng), mp.RealMatrix.zeros(n, n, k))
+    C = mp.cgemm_3m(A, B)
+    assert np.all(C.im_plane.data == 0.0)
+    assert C.re_plane.bitwise_equal(mp.cgemm_4m(A, B).re_plane)
+    ints = rng.integers(-100, 100, size=(6, 6)).astype(float)
+    A = mp.PlanarComplexMatrix(mp.RealMatrix.from_float64(ints, 2), mp.RealMatrix.zeros(6, 6, 2))
+    iI = mp.PlanarComplexMatrix(mp.RealMatrix.zeros(6, 6, 2), mp.RealMatrix.identity(6, 2))
+    C = mp.cgemm_4m(iI, A, mp.KernelChoice(method="4m", real_kernel="naive"))
+    assert np.all(C.re_plane.data == 0.0)
+    assert np.array_equal(C.im_plane.data[0], ints)
+
+
+def test_kernel_call_counts():
+    rng = np.random.default_rng(1)
+    A = pc(*rand_pc(rng, 8, 8, 2))
+    for kern in ("naive", "blocked", "b200"):
+        mp.reset_real_kernel_calls()
+        mp.cgemm_3m(A, A, mp.KernelChoice(method="3m", real_kernel=kern))
+        assert mp.real_kernel_calls()[kern] == 3
+        mp.reset_real_kernel_calls()
+        mp.cgemm_4m(A, A, mp.KernelChoice(method="4m", real_kernel=kern))
+        assert mp.real_kernel_calls()[kern] == 4
+
+
+@pytest.mark.parametrize("k,cases", [
+    (2, [(1, 1), (2, 2), (33, 7), (33, 33), (100, 16), (130, 32), (130, 1), (257, 64)]),
+    (3, [(19, 5), (40, 16), (65, 32)]),
+    (4, [(19, 5), (40, 16)]),
+])
+def test_lu_vs_oracle(orc, k, cases):
+    for n, K in cases:
+        for meth in ("3m", "4m"):
+            rng = np.random.default_rng(n * 131 + K)
+            re, im = problems.lu_matrix(n, k, n + K, populate_lower=k > 2,
+                                        renorm=orc.renorm_planes)
+            if n > 4:  # integer-valued rows create exact pivot ties
+                re[0, 1::3] = np.round(re[0, 1::3] * 4)
+                im[0, 1::3] = np.round(im[0, 1::3] * 4)
+                re[1:, 1::3] = 0.0
+                im[1:, 1::3] = 0.0
+            fr, fi, piv, st = orc.factor(re, im, K, meth)
+            f = mp.lu_blocked(pc(re, im), K, kc=mp.KernelChoice(method=meth))
+            assert st == -1
+            assert np.array_equal(f.pivots, piv), (n, K, meth)
+            assert beq(f.packed.re_plane.data, fr), (n, K, meth, first_diff(f.packed.re_plane.data, fr))
+            assert beq(f.packed.im_plane.data, fi), (n, K, meth)
+
+
+# ------------------------------------------------------- BASELINE configs
+
+def test_cfg0_digests_and_errors():
+    path = os.path.join(GOLD, "cfg0.json")
+    cases = json.load(open(path))["cases"]
+    for c in cases:
+        re, im = problems.lu_matrix(c["n"], c["k"], c["seed"])
+        A = pc(re, im)
+        if c["K"] == c["n"]:
+            f = mp.lu_normal(A, method=c["method"])
+        else:
+            f = mp.lu_blocked(A, c["K"], kc=mp.KernelChoice(method=c["method"]))
+        assert [int(p) for p in f.pivots] == c["pivots"]
+        assert digest(f.packed.re_plane.data, f.packed.im_plane.data) == c["digest"]
+        # b = cgemm_4m(A, x_true) (naive) is the same chain on the GPU
+        xr, xi = problems.x_true(c["n"], c["k"])
+        X = pc(xr.reshape(c["k"], c["n"], 1).copy(), xi.reshape(c["k"], c["n"], 1).copy())
+        B = mp.cgemm_4m(A, X, mp.KernelChoice(method="4m", real_kernel="naive"))
+        b = np.array([B.re_plane.data[:, :, 0], B.im_plane.data[:, :, 0]])
+        assert digest(b) == c["b_digest"]
+        x = mp.solve(f, mp.ComplexVector(b[0], b[1]))
+        fwd = mp.max_rel_err(x, mp.ComplexVector(xr, xi))
+        assert fwd <= 10 * c["n"] * U_PREC[c["k"]] * 100, fwd
+        assert fwd <= max(10 * c["fwd_err"], 1e-28)
+
+
+def test_cfg1_gemm_digest():
+    path = os.path.join(GOLD, "cfg1.json")
+    g = json.load(open(path))
+    n, k = 1024, 2
+    a, b = problems.gemm_inputs(n, k, 1, mp.renorm_planes)
+    assert digest(a[0], a[1], b[0], b[1]) == g["input_digest"]
+    for c in g["cases"]:
+        C = mp.cgemm(pc(*a), pc(*b), mp.KernelChoice(method=c["method"]))
+        assert digest(C.re_plane.data, C.im_plane.data) == c["digest"], c["method"]
+
+
+def test_cfg2_lu_digest():
+    path = os.path.join(GOLD, "cfg2.json")
+    if not os.path.exists(path):
+        pytest.skip("cfg2 golden not generated")
+    g = json.load(open(path))
+    c = g["cases"][0]
+    re, im = problems.lu_matrix(c["n"], c["k"], c["seed"])
+    assert digest(re, im) == g["input_digest"]
+    f = mp.lu_blocked(pc(re, im), c["K"], kc=mp.KernelChoice(method=c["method"]))
+    assert [int(p) for p in f.pivots] == c["pivots"]
+    assert digest(f.packed.re_plane.data, f.packed.im_plane.data) == c["digest"]
