@@ -117,8 +117,9 @@ int mpc_getrs(int k, int method, int64_t n, const double* re, const double* im,
               const int64_t* piv, double* b_re, double* b_im, void* stream);
 
 /* ---- measurement hooks (bench.py) ---- */
-/* Enable/disable per-launch CUDA-event timing (clears previous records). */
-void mpc_prof_enable(int on);
+/* Per-launch CUDA-event timing of the kernel classes whose bit is set in
+ * `mask` (bit c = class c below; 0 disables).  Clears previous records. */
+void mpc_prof_enable(int mask);
 /* Sum per kernel class (0 GEMM, 1 S-update, 2 panel, 3 TRSM diagonal,
  * 4 LASWP, 5 other) of event-timed ms, algorithmic FP64 ops (op model v1)
  * and launch counts since the last mpc_prof_enable(1).  Returns the number of

@@ -93,8 +93,15 @@ def ptr(a):
     return a.data_ptr()  # torch.Tensor
 
 
-def prof_enable(on=True):
-    lib().mpc_prof_enable(1 if on else 0)
+def prof_enable(on=True, classes=None):
+    """Event-time every launch of the given classes (default: all)."""
+    if not on:
+        mask = 0
+    elif classes is None:
+        mask = (1 << len(PROF_CLASSES)) - 1
+    else:
+        mask = sum(1 << PROF_CLASSES.index(c) for c in classes)
+    lib().mpc_prof_enable(mask)
 
 
 def prof_summary():

@@ -23,7 +23,7 @@ OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libmpcb200.so")
 
 SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "abi.cu"]
-HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h"]
+HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -46,8 +46,9 @@ def _stale(out, deps):
 
 def _compile(src, verbose):
     obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
-    deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [
-        os.path.join(os.path.dirname(HERE), "include", "mpc_b200.h"), __file__]
+    deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
+    if src == "abi.cu":
+        deps.append(os.path.join(os.path.dirname(HERE), "include", "mpc_b200.h"))
     if not _stale(obj, deps):
         return obj, ""
     cmd = [nvcc()] + ARCH + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + [

@@ -27,6 +27,7 @@ struct ProfRec {
 struct ProfState {
   std::mutex mu;
   bool on = false;
+  int mask = 0;
   std::atomic<long long> launches{0};
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
@@ -50,7 +51,7 @@ ProfState& P() {
 int prof_begin(int cls, double ops, cudaStream_t st) {
   ProfState& p = P();
   p.launches++;
-  if (!p.on) return -1;
+  if (!p.on || !((p.mask >> cls) & 1)) return -1;
   std::lock_guard<std::mutex> g(p.mu);
   ProfRec r{cls, ops, p.get(), p.get()};
   cudaEventRecord(r.a, st);
@@ -263,6 +264,7 @@ void mpc_prof_enable(int on) {
   }
   p.recs.clear();
   p.on = on != 0;
+  p.mask = on;
 }
 
 long long mpc_launch_count(void) { return mpc::P().launches.load(); }
