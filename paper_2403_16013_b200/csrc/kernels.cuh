@@ -809,18 +809,53 @@ struct Ops {
     laswp(A, jb + kw, n - jb - kw, piv, jb, jb + kw, st, ws.status);
   }
 
-  // lu._factor (lu.py:129-163), everything on `st`
+  // Trailing work of panel b = [jb, jb+kw) on the column range [c0, c1)
+  // (all right of the panel): interchanges, U12 TRSM, fused A22 -= L21 U12.
+  static void update_cols(bool use3m, View A, int64_t n, int64_t jb, int64_t kw, int64_t c0,
+                          int64_t c1, const int64_t* piv, const int64_t* status,
+                          cudaStream_t st) {
+    if (c1 <= c0) return;
+    int64_t end = jb + kw;
+    laswp(A, c0, c1 - c0, piv, jb, end, st, status);
+    trsm(use3m, kw, c1 - c0, A.sub(jb, jb), A.sub(jb, c0), st, status);
+    cgemm(use3m, n - end, kw, c1 - c0, A.sub(end, jb), A.sub(jb, c0), A.sub(end, c0), 1, st,
+          status);
+  }
+
+  // lu._factor (lu.py:129-163) with depth-1 lookahead: while `st` applies
+  // panel b's trailing update to columns right of block b+1, panel b+1
+  // (already updated by b) is factored on a high-priority side stream.
+  // Element operation sequences are unchanged (bit-identical to the
+  // sequential schedule); only independent column ranges overlap.
   static void getrf(bool use3m, View A, int64_t n, int64_t Kp, int64_t* piv, PanelWs ws,
                     cudaStream_t st) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStream_t sp;
+    cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi);
+    cudaEvent_t ev_narrow, ev_panel;
+    cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+    panel_rec(use3m, A, n, 0, std::min(Kp, n), piv, ws, st);
     for (int64_t jb = 0; jb < n; jb += Kp) {
       int64_t kw = std::min(Kp, n - jb);
-      lu_panel(use3m, A, n, jb, kw, piv, ws, st);
       int64_t end = jb + kw;
+      laswp(A, 0, jb, piv, jb, end, st, ws.status);  // left of the panel
       if (end == n) break;
-      int64_t M = n - end;
-      trsm(use3m, kw, M, A.sub(jb, jb), A.sub(jb, end), st, ws.status);
-      cgemm(use3m, M, kw, M, A.sub(end, jb), A.sub(jb, end), A.sub(end, end), 1, st, ws.status);
+      int64_t kw2 = std::min(Kp, n - end);
+      // narrow update of block b+1, then factor it on the side stream
+      update_cols(use3m, A, n, jb, kw, end, end + kw2, piv, ws.status, st);
+      cudaEventRecord(ev_narrow, st);
+      cudaStreamWaitEvent(sp, ev_narrow, 0);
+      panel_rec(use3m, A, n, end, kw2, piv, ws, sp);
+      cudaEventRecord(ev_panel, sp);
+      // rest of panel b's update overlaps the panel factorization
+      update_cols(use3m, A, n, jb, kw, end + kw2, n, piv, ws.status, st);
+      cudaStreamWaitEvent(st, ev_panel, 0);
     }
+    cudaEventDestroy(ev_narrow);
+    cudaEventDestroy(ev_panel);
+    cudaStreamDestroy(sp);
   }
 
   static constexpr int SOLVE_BLOCK = 32;
