@@ -514,26 +514,45 @@ __global__ void laswp_kernel(View A, int64_t col0, int64_t ncols, const int64_t*
 }
 
 // -------------------------------------------------------------- TRSM
-// Diagonal block of trsm_ll_unit (_kernels.py:687-705): one thread per
-// column, rows r ascending, subtractions s ascending.
+// Diagonal block of trsm_ll_unit (_kernels.py:687-705), right-looking and
+// lane-parallel: a group of 16 lanes owns one column, lane r holds x_r.  At
+// step s lane s's value is final (all its subtractions s' < s are done); it
+// is broadcast by shuffle and every lane r > s applies x_r -= cmul(L_rs, x_s).
+// Each x_r therefore receives exactly the reference's chain (s ascending).
+constexpr int TRSM_BASE_MAX = 16;
+template <int K>
+MPC_DI Exp<K> shfl_exp(const Exp<K>& v, int src) {
+  Exp<K> o;
+#pragma unroll
+  for (int q = 0; q < K; q++) o.c[q] = __shfl_sync(0xffffffffu, v.c[q], src, TRSM_BASE_MAX);
+  return o;
+}
+
 template <int K>
 __global__ void trsm_diag_kernel(View L, View X, int64_t kb, int64_t M, int use3m,
                                  const int64_t* status) {
   if (status != nullptr && *status >= 0) return;
-  int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= M) return;
-  for (int64_t r = 1; r < kb; r++) {
-    Exp<K> xr = ldexp_<K>(X.re + r * X.ld + col, X.ps);
-    Exp<K> xi = ldexp_<K>(X.im + r * X.ld + col, X.ps);
-    for (int64_t s = 0; s < r; s++) {
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int r = (int)(gid % TRSM_BASE_MAX);
+  int64_t col = gid / TRSM_BASE_MAX;
+  bool live = col < M && r < kb;  // whole 16-lane groups share a column
+  Exp<K> xr = exp_zero<K>(), xi = exp_zero<K>();
+  if (live) {
+    xr = ldexp_<K>(X.re + r * X.ld + col, X.ps);
+    xi = ldexp_<K>(X.im + r * X.ld + col, X.ps);
+  }
+  for (int s = 0; s + 1 < (int)kb; s++) {
+    Exp<K> yr = shfl_exp<K>(xr, s);
+    Exp<K> yi = shfl_exp<K>(xi, s);
+    if (live && r > s) {
       Exp<K> lr = ldexp_<K>(L.re + r * L.ld + s, L.ps);
       Exp<K> li = ldexp_<K>(L.im + r * L.ld + s, L.ps);
-      Exp<K> yr = ldexp_<K>(X.re + s * X.ld + col, X.ps);
-      Exp<K> yi = ldexp_<K>(X.im + s * X.ld + col, X.ps);
       Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
       xr = exp_sub(xr, p.re);
       xi = exp_sub(xi, p.im);
     }
+  }
+  if (live && r > 0) {
     stexp_<K>(X.re + r * X.ld + col, X.ps, xr);
     stexp_<K>(X.im + r * X.ld + col, X.ps, xi);
   }
@@ -743,14 +762,15 @@ struct Ops {
     check_launch("laswp_kernel");
   }
 
-  static constexpr int TRSM_BASE = 16;
+  static constexpr int TRSM_BASE = TRSM_BASE_MAX;
   // L (kb x kb, unit lower, strictly-lower part read) and X (kb x M) views
   static void trsm(bool use3m, int64_t kb, int64_t M, View L, View X, cudaStream_t st,
                    const int64_t* status) {
     if (kb <= 1 || M <= 0) return;
     if (kb <= TRSM_BASE) {
       int tok_ = prof_begin(PC_TRSM, (double)M * (double)(kb * (kb - 1) / 2) * OpModel<K>::upd(use3m), st);
-      trsm_diag_kernel<K><<<cdiv_u(M, 128), 128, 0, st>>>(L, X, kb, M, use3m ? 1 : 0, status);
+      trsm_diag_kernel<K><<<cdiv_u(M * TRSM_BASE_MAX, 128), 128, 0, st>>>(L, X, kb, M,
+                                                                            use3m ? 1 : 0, status);
       prof_end(tok_, st);
       check_launch("trsm_diag_kernel");
       return;
