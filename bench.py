@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "complex-DD LU GFLOPS (8n³/3 conv.) & % FP64 peak at 1/2/4/8 B200 vs host CPU"
-CPU_SAMPLE_N = 1536
+CPU_SAMPLE_N = 2048
 
 
 def parse():
@@ -41,7 +41,9 @@ def parse():
     p.add_argument("--steps", type=int, default=2)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--workload", default="lu", choices=["lu", "gemm"],
+                   help="lu: config 4 (headline); gemm: config 1 complex DD GEMM")
+    p.add_argument("--n", type=int, default=None)
     p.add_argument("--K", type=int, default=512)
     p.add_argument("--k", type=int, default=2)
     p.add_argument("--method", default="3m", choices=["3m", "4m"])
@@ -312,8 +314,69 @@ def run_b200(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+def run_gemm(args):
+    """Config 1: C = A B, complex DD, both limbs populated, n = 1024 default.
+    Inputs (96 MiB) fit in L2, so a 512 MiB buffer is written between timed
+    GEMMs (outside the per-GEMM events) to flush it."""
+    import torch
+
+    import paper_2403_16013_b200 as mp
+    from paper_2403_16013_b200 import _lib, device, problems
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n, k = args.n, args.k
+    a, b = problems.gemm_inputs(n, k, args.seed, mp.renorm_planes)
+    T = [torch.from_numpy(x).to(dev) for x in (a[0], a[1], b[0], b[1])]
+    cr = torch.empty((k, n, n), dtype=torch.float64, device=dev)
+    ci = torch.empty_like(cr)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def gemm():
+        device.cgemm(*T, cr, ci, method=args.method)
+
+    for _ in range(args.warmup):
+        gemm()
+    torch.cuda.synchronize()
+    peak = device.fp64_peak()
+    l0 = _lib.launch_count()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gemm()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - l0
+    ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    ms_step = statistics.mean(ms)
+    ops = n ** 3 * (93 if args.method == "3m" else 124) * (1 if k == 2 else 0)
+    ach = ops / (ms_step * 1e-3) / 1e12
+    from paper_2403_16013_b200.digest import digest
+
+    out = {"metric": "complex-DD GEMM GFLOPS (8n³ conv.) & % FP64 peak", "value":
+           8.0 * n ** 3 / (ms_step * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (DD)",
+           "data": "synthetic", "config": {"workload": f"cfg1: complex DD GEMM n={n} {args.method}",
+                                            "l2": "512 MiB buffer written between timed GEMMs"},
+           "roofline": {"bound": "fp64", "achieved": ach, "peak": peak / 1e12, "frac":
+                        ach * 1e12 / peak, "unit": "TFLOP/s (FP64 instr/s)", "traffic": None},
+           "gemm_variant": os.environ.get("MPC_GEMM_VARIANT", "0"),
+           "digest": digest(cr.cpu().numpy(), ci.cpu().numpy()), "gpu_launches": launches}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
+    if args.n is None:
+        args.n = 1024 if args.workload == "gemm" else 16384
+    if args.workload == "gemm" and args.impl == "b200":
+        return run_gemm(args)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if args.impl == "reference":

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <algorithm>
+#include <cstdlib>
 #include "expansion.cuh"
 #include "prof.h"
 
@@ -95,8 +96,8 @@ struct GemmCfg {
   static constexpr size_t SMEM = sizeof(double) * 2 * (A_STAGE + B_STAGE);
 };
 
-template <int K, int MODE, int BM, int BN, int BK, int TM, int TN>
-__global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT)
+template <int K, int MODE, int BM, int BN, int BK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB)
     gemm_kernel(GemmArgs g) {
   using Cfg = GemmCfg<K, MODE, BM, BN, BK, TM, TN>;
   using MI = ModeInfo<MODE>;
@@ -687,22 +688,43 @@ struct Ops {
   static constexpr int TM = (K == 2) ? 2 : 1;
   static constexpr int TN = (K == 2) ? 2 : 1;
 
-  template <int MODE>
-  static void gemm_launch(const GemmArgs& g, cudaStream_t st, int MI_CLASS, double per_elem) {
-    if (g.m <= 0 || g.l <= 0) return;
-    double ops = (double)g.m * (double)g.l * (double)g.n * per_elem;
-    using Cfg = GemmCfg<K, MODE, BM, BN, BK, TM, TN>;
-    auto kern = gemm_kernel<K, MODE, BM, BN, BK, TM, TN>;
+  template <int MODE, int BM_, int BN_, int BK_, int TM_, int TN_, int MINB_>
+  static void launch_cfg(const GemmArgs& g, cudaStream_t st, int cls, double ops) {
+    using Cfg = GemmCfg<K, MODE, BM_, BN_, BK_, TM_, TN_>;
+    auto kern = gemm_kernel<K, MODE, BM_, BN_, BK_, TM_, TN_, MINB_>;
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
       attr_set = true;
     }
-    dim3 grid(cdiv_u(g.l, BN), cdiv_u(g.m, BM));
-    int tok_ = prof_begin(MI_CLASS, ops, st);
+    dim3 grid(cdiv_u(g.l, BN_), cdiv_u(g.m, BM_));
+    int tok_ = prof_begin(cls, ops, st);
     kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(g);
     prof_end(tok_, st);
     check_launch("gemm_kernel");
+  }
+
+  // tile variant for K = 2 (MPC_GEMM_VARIANT, read once)
+  static int variant() {
+    static int v = [] {
+      const char* e = getenv("MPC_GEMM_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
+    return v;
+  }
+
+  template <int MODE>
+  static void gemm_launch(const GemmArgs& g, cudaStream_t st, int cls, double per_elem) {
+    if (g.m <= 0 || g.l <= 0) return;
+    double ops = (double)g.m * (double)g.l * (double)g.n * per_elem;
+    if constexpr (K == 2) {
+      switch (variant()) {
+        case 1: launch_cfg<MODE, 32, 32, 8, 2, 2, 3>(g, st, cls, ops); return;
+        case 2: launch_cfg<MODE, 32, 32, 16, 2, 2, 2>(g, st, cls, ops); return;
+        default: break;
+      }
+    }
+    launch_cfg<MODE, BM, BN, BK, TM, TN, (K == 2 ? 2 : 1)>(g, st, cls, ops);
   }
 
   static void rgemm(int64_t m, int64_t n, int64_t l, View a, View b, View c, cudaStream_t st) {
