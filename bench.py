@@ -62,7 +62,8 @@ def conv_flops(n):
 
 def workload(args):
     prec = {2: "DD", 3: "TD", 4: "QD"}[args.k]
-    tag = "cfg4" if (args.n, args.K, args.k) == (16384, 512, 2) else "custom"
+    tag = {(16384, 512, 2): "cfg4", (4096, 256, 2): "cfg2", (128, 128, 2): "cfg0",
+           (2048, 128, 3): "cfg3", (2048, 128, 4): "cfg3"}.get((args.n, args.K, args.k), "custom")
     return (f"{tag}: complex {prec} blocked LU with partial pivoting, n={args.n}, K={args.K}, "
             f"{args.method.upper()} trailing update" + (", ill-conditioned rows" if args.ill else ""))
 
@@ -187,7 +188,10 @@ def run_b200(args, rank, world):
     torch.cuda.set_device(dev)
     _lib.require_device()
     n, K, k = args.n, args.K, args.k
-    re0, im0 = problems.lu_matrix(n, k, args.seed, ill_conditioned=args.ill)
+    # configs 0/2/4: lower limbs 0; config 3 (k > 2): every limb populated
+    re0, im0 = problems.lu_matrix(n, k, args.seed, populate_lower=k > 2,
+                                  renorm=mp.renorm_planes if k > 2 else None,
+                                  ill_conditioned=args.ill)
 
     if world > 1:
         from paper_2403_16013_b200 import dist

@@ -23,7 +23,7 @@ OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libmpcb200.so")
 
 SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "abi.cu"]
-HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h"]
+HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -9,13 +9,15 @@
 //   * the only DFMA is TwoProd's error term, fma(a,b,-a*b), which equals the
 //     reference's Dekker error term exactly for in-range operands;
 //   * the k>=3 renormalization keeps the reference's data-dependent control
-//     flow (stable sort by (|v| desc, v desc), VecSum, extraction with early
-//     break, repeat-while-overlapping <= 6) using predication instead of
-//     dynamic indexing so everything stays in registers.
+//     flow (sort by (|v| desc, v desc), VecSum, extraction with early break,
+//     repeat-while-overlapping <= 6) using a sorting network and predication
+//     instead of dynamic indexing so everything stays in registers.
 // Comparisons that only steer control flow are done on the integer pipe
 // (bit patterns) to keep the FP64 pipe for arithmetic.
 #pragma once
 #include <cstdint>
+
+#include "sortnet.h"
 
 namespace mpc {
 
@@ -98,35 +100,36 @@ MPC_DI Exp<K> exp_abs(const Exp<K>& x) {
   return (x.c[0] < 0.0) ? exp_neg(x) : x;
 }
 
-// sort key for (|v| desc, v desc): equal keys <=> the reference's insertion
-// sort would not move one past the other (+0 and -0 compare equal there).
+// sort key for (|v| desc, v desc), offset by one so that 0 can mark padding
+// slots: equal keys <=> identical values, or zeros of either sign (the
+// reference's insertion sort does not order +0 / -0 either).
 MPC_DI uint64_t sort_key(double v) {
   uint64_t a = absbits(v);
   uint64_t pos = (a != 0ull && !(bits(v) >> 63)) ? 1ull : 0ull;
-  return (a << 1) | pos;
+  return ((a << 1) | pos) + 1ull;
 }
 
-// _sort_desc, _kernels.py:67-78.  Insertion sort written as the equivalent
-// bubble network of strict compare-exchanges (stable, same permutation),
-// restricted to the first m entries (m <= M, runtime).
+// _sort_desc, _kernels.py:67-78, on buf[0..m) (m <= M, runtime).  A sorting
+// network (sortnet.h) replaces the insertion sort: the sorted sequence is
+// the same except for the relative order of equal keys, i.e. identical
+// values (no effect) or signed zeros, which always form the tail and whose
+// order cannot change the VecSum sweep (every TwoSum of two zeros yields the
+// same sum and a +0 error irrespective of order) -- so renorm's output is
+// bit-identical.  Padding slots (i >= m) get key 0 and sink to the end.
 template <int M>
 MPC_DI void sort_desc(double (&buf)[M], int m) {
   uint64_t key[M];
 #pragma unroll
-  for (int i = 0; i < M; i++) key[i] = sort_key(buf[i]);
-#pragma unroll
-  for (int i = 1; i < M; i++) {
-#pragma unroll
-    for (int j = i - 1; j >= 0; j--) {
-      bool sw = (i < m) && (key[j] < key[j + 1]);
-      double a = buf[j], b = buf[j + 1];
-      uint64_t ka = key[j], kb = key[j + 1];
-      buf[j] = sw ? b : a;
-      buf[j + 1] = sw ? a : b;
-      key[j] = sw ? kb : ka;
-      key[j + 1] = sw ? ka : kb;
-    }
-  }
+  for (int i = 0; i < M; i++) key[i] = (i < m) ? sort_key(buf[i]) : 0ull;
+  SortNet<M>::apply([&](int a, int b) {
+    bool sw = key[a] < key[b];
+    double va = buf[a], vb = buf[b];
+    uint64_t ka = key[a], kb = key[b];
+    buf[a] = sw ? vb : va;
+    buf[b] = sw ? va : vb;
+    key[a] = sw ? kb : ka;
+    key[b] = sw ? ka : kb;
+  });
 }
 
 // _vecsum_extract, _kernels.py:81-105, on buf[0..m) (m <= M runtime)

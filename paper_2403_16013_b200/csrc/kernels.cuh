@@ -23,6 +23,8 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
+#include <vector>
 #include "expansion.cuh"
 #include "prof.h"
 
@@ -684,7 +686,9 @@ struct Ops {
   // tile configurations (tuned per K)
   static constexpr int BM = (K == 2) ? 32 : 16;
   static constexpr int BN = (K == 2) ? 32 : 16;
-  static constexpr int BK = 8;
+  // K=2: BK=16 measured best (cfg1 n=1024: 89.8% of FP64 peak vs 86.9% at
+  // BK=8; profiles/r1_gemm_variants.txt)
+  static constexpr int BK = (K == 2) ? 16 : 8;
   static constexpr int TM = (K == 2) ? 2 : 1;
   static constexpr int TN = (K == 2) ? 2 : 1;
 
@@ -719,8 +723,7 @@ struct Ops {
     double ops = (double)g.m * (double)g.l * (double)g.n * per_elem;
     if constexpr (K == 2) {
       switch (variant()) {
-        case 1: launch_cfg<MODE, 32, 32, 8, 2, 2, 3>(g, st, cls, ops); return;
-        case 2: launch_cfg<MODE, 32, 32, 16, 2, 2, 2>(g, st, cls, ops); return;
+        case 1: launch_cfg<MODE, 32, 32, 8, 2, 2, 2>(g, st, cls, ops); return;  // round-1 v0
         default: break;
       }
     }
@@ -878,7 +881,19 @@ struct Ops {
     cudaEvent_t ev_narrow, ev_panel;
     cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+    // MPC_TRACE=1: per-step timeline (stderr) -- where the step time goes
+    static const bool trace = getenv("MPC_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t s) {
+      if (!trace) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      tev.push_back(e);
+    };
+    mark(st);
     panel_rec(use3m, A, n, 0, std::min(Kp, n), piv, ws, st);
+    mark(st);
     for (int64_t jb = 0; jb < n; jb += Kp) {
       int64_t kw = std::min(Kp, n - jb);
       int64_t end = jb + kw;
@@ -888,12 +903,33 @@ struct Ops {
       // narrow update of block b+1, then factor it on the side stream
       update_cols(use3m, A, n, jb, kw, end, end + kw2, piv, ws.status, st);
       cudaEventRecord(ev_narrow, st);
+      mark(st);
       cudaStreamWaitEvent(sp, ev_narrow, 0);
       panel_rec(use3m, A, n, end, kw2, piv, ws, sp);
       cudaEventRecord(ev_panel, sp);
+      mark(sp);
       // rest of panel b's update overlaps the panel factorization
       update_cols(use3m, A, n, jb, kw, end + kw2, n, piv, ws.status, st);
+      mark(st);
       cudaStreamWaitEvent(st, ev_panel, 0);
+      mark(st);
+    }
+    if (trace) {
+      cudaStreamSynchronize(st);
+      float t;
+      cudaEventElapsedTime(&t, tev[0], tev[1]);
+      fprintf(stderr, "MPC_TRACE n=%lld K=%lld first-panel %.3f ms\n", (long long)n, (long long)Kp, t);
+      // per step: [start(prev end), narrow done, panel done (side), rest done, joined]
+      for (size_t i = 1; i + 4 < tev.size(); i += 4) {
+        float tn, tp, tr, tj;
+        cudaEventElapsedTime(&tn, tev[i], tev[i + 1]);
+        cudaEventElapsedTime(&tp, tev[i + 1], tev[i + 2]);
+        cudaEventElapsedTime(&tr, tev[i + 1], tev[i + 3]);
+        cudaEventElapsedTime(&tj, tev[i], tev[i + 4]);
+        fprintf(stderr, "MPC_TRACE step %zu: narrow %.3f  panel(side) %.3f  rest %.3f  step %.3f ms\n",
+                (i - 1) / 4, tn, tp, tr, tj);
+      }
+      for (auto e : tev) cudaEventDestroy(e);
     }
     cudaEventDestroy(ev_narrow);
     cudaEventDestroy(ev_panel);

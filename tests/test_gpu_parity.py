@@ -264,3 +264,22 @@ def test_cfg2_lu_digest():
     f = mp.lu_blocked(pc(re, im), c["K"], kc=mp.KernelChoice(method=c["method"]))
     assert [int(p) for p in f.pivots] == c["pivots"]
     assert digest(f.packed.re_plane.data, f.packed.im_plane.data) == c["digest"]
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_cfg3_lu_digest(k):
+    """BASELINE config 3: TD / QD LU n=2048, K=128, 3M and 4M, every limb
+    populated -- pivots and packed factors against the reference's digests."""
+    path = os.path.join(GOLD, "cfg3_n2048.json")
+    if not os.path.exists(path):
+        pytest.skip("cfg3 golden not generated")
+    g = json.load(open(path))
+    cases = [c for c in g["cases"] if c["k"] == k]
+    if not cases:
+        pytest.skip(f"cfg3 k={k} golden not generated")
+    re, im = problems.lu_matrix(2048, k, 1, populate_lower=True, renorm=mp.renorm_planes)
+    assert digest(re, im) == cases[0]["input_digest"]
+    for c in cases:
+        f = mp.lu_blocked(pc(re, im), c["K"], kc=mp.KernelChoice(method=c["method"]))
+        assert [int(p) for p in f.pivots] == c["pivots"], c["method"]
+        assert digest(f.packed.re_plane.data, f.packed.im_plane.data) == c["digest"], c["method"]
