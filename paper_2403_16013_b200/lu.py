@@ -239,3 +239,63 @@ def factor_inplace(re, im, K, method="3m", piv=None):
     if st >= 0:
         raise SingularMatrixError(int(st))
     return piv
+
+
+def _promote(M, k_new):
+    return PlanarComplexMatrix(M.re_plane.promote(k_new), M.im_plane.promote(k_new))
+
+
+def reconstruction_error(f, A, threads=8, extra=2):
+    """max componentwise |PA - LU| over both planes (lu.py:236-250), with the
+    L U product at k + extra components through the GPU kernel.  The device
+    path stops at k = 4, so this is available for DD factors (extra = 2)."""
+    from .cmatrix import cgemm
+
+    kk = f.packed.k + extra
+    if kk > 4:
+        raise NotImplementedError("reconstruction at k > 4 is not on the B200 path yet")
+    from .rmatrix import mat_sub
+
+    PA = _promote(permuted(A, f.pivots), kk)
+    L = _promote(f.lower(), kk)
+    U = _promote(f.upper(), kk)
+    LU = cgemm(L, U, KernelChoice(method="3m", real_kernel="blocked", threads=threads))
+    dre = mat_sub(PA.re_plane, LU.re_plane)
+    dim = mat_sub(PA.im_plane, LU.im_plane)
+    return max(dre.max_abs(), dim.max_abs())
+
+
+def backward_error_probe(f, A, seed=0):
+    """O(n^2) estimate of the normwise backward error ||PA - LU|| / ||A||
+    (infinity norm, |Re| + |Im| moduli): r = P A v - L (U v) for a seeded
+    random DD vector v, evaluated in quad-double (k + 2 = 4) with the GPU
+    GEMM at l = 1.  Returns ||r|| / (||A|| ||v||), a lower bound of the
+    normwise backward error, for DD factors."""
+    from .cmatrix import cgemm
+
+    k, n = f.packed.k, f.n
+    if k != 2:
+        raise NotImplementedError("probe needs k + 2 <= 4")
+    rng = np.random.Generator(np.random.Philox(key=np.uint64(seed + 12345)))
+    v = np.zeros((2, 4, n, 1))
+    v[0, 0, :, 0] = rng.uniform(-1, 1, n)
+    v[1, 0, :, 0] = rng.uniform(-1, 1, n)
+    V = PlanarComplexMatrix(RealMatrix(v[0]), RealMatrix(v[1]))
+    kc = KernelChoice(method="4m")
+    PA = _promote(permuted(A, f.pivots), 4)
+    y3 = cgemm(PA, V, kc)
+    del PA
+    U = _promote(f.upper(), 4)
+    y1 = cgemm(U, V, kc)
+    del U
+    L = _promote(f.lower(), 4)
+    y2 = cgemm(L, y1, kc)
+    del L
+    from .rmatrix import mat_sub
+
+    rr = mat_sub(y3.re_plane, y2.re_plane).data
+    ri = mat_sub(y3.im_plane, y2.im_plane).data
+    rnorm = float(np.max(np.abs(rr[0]) + np.abs(ri[0])))
+    anorm = float(np.max(np.sum(np.abs(A.re_plane.data[0]) + np.abs(A.im_plane.data[0]), axis=1)))
+    vnorm = float(np.max(np.abs(v[0, 0]) + np.abs(v[1, 0])))
+    return rnorm / (anorm * vnorm)
