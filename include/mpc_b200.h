@@ -92,11 +92,20 @@ int64_t mpc_lu_panel(int k, int method, int64_t n, double* re, double* im, int64
 
 /* The same panel elimination restricted to the panel's own columns (the
  * interchanges are NOT applied outside [jb, jb+kw); apply them with
- * mpc_laswp).  Element (i, c), c in [jb, jb+kw), is at re[i*ld + c]; used by
- * the column-distributed multi-GPU driver.  Synchronous. */
+ * mpc_laswp).  re/im point at element (0, jb) of the matrix: element
+ * (i, jb + t), 0 <= t < kw, is at re[i*ld + t]; rows [jb, n) are factored and
+ * piv[jb .. jb+kw) (absolute row numbers) is written.  Used by the
+ * column-distributed multi-GPU driver.  Synchronous. */
 int64_t mpc_panel_factor(int k, int method, int64_t n, int64_t jb, int64_t kw,
                          double* re, double* im, int64_t ld, int64_t ps, int64_t* piv,
                          void* stream);
+
+/* Asynchronous variant (device pointers only): enqueues the panel on
+ * `stream` and writes the status (-1 or the singular column) to the device
+ * word *status_out instead of returning it; returns 0 or MPC_ERR. */
+int mpc_panel_factor_async(int k, int method, int64_t n, int64_t jb, int64_t kw,
+                           double* re, double* im, int64_t ld, int64_t ps, int64_t* piv,
+                           int64_t* status_out, void* stream);
 
 /* Apply the interchanges piv[r0..r1) in order to columns [0, ncols) of a
  * (rows x ncols) view (the deferred part of _swap_rows, _kernels.py:597-608). */

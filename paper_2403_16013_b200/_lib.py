@@ -29,6 +29,7 @@ _SIGS = {
     "mpc_trsm_ll_unit": (_i, [_i, _i, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _i64, _i64, _p]),
     "mpc_lu_panel": (_i64, [_i, _i, _i64, _p, _p, _p, _i64, _i64, _p]),
     "mpc_panel_factor": (_i64, [_i, _i, _i64, _i64, _i64, _p, _p, _i64, _i64, _p, _p]),
+    "mpc_panel_factor_async": (_i, [_i, _i, _i64, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _p]),
     "mpc_laswp": (_i, [_i, _i64, _p, _p, _i64, _i64, _p, _i64, _i64, _p]),
     "mpc_getrf": (_i64, [_i, _i, _i64, _i64, _p, _p, _p, _p]),
     "mpc_getrs": (_i, [_i, _i, _i64, _p, _p, _p, _p, _p, _p]),

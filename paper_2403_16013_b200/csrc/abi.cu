@@ -428,18 +428,45 @@ int64_t mpc_panel_factor(int k, int method, int64_t n, int64_t jb, int64_t kw, d
   cudaStream_t st = (cudaStream_t)stream;
   Stager sg(st);
   if (!sg.classify({re, im, piv})) return MPC_ERR;
-  int64_t e = extent(k, n, jb + kw, ld, ps);
+  // re/im point at element (0, jb): column jb + t is at re[i*ld + t]
+  int64_t e = extent(k, n, kw, ld, ps);
   double* dr = sg.map(re, e, true, true);
   double* di = sg.map(im, e, true, true);
   int64_t* dp = sg.map(piv, n, true, true);
   int64_t status = -1;
   if (kw > 0) {
     WsHolder w(k, n, st);
-    table_for(k)->panel_rec(method == 3, mpc::View{dr, di, ld, ps}, n, jb, kw, dp, w.ws, st);
+    // shift so that global column indices address the panel (never
+    // dereferenced left of column jb)
+    table_for(k)->panel_rec(method == 3, mpc::View{dr - jb, di - jb, ld, ps}, n, jb, kw, dp,
+                            w.ws, st);
     status = w.read_status();
   }
   sg.finish();
   return status;
+  MPC_CATCH
+}
+
+int mpc_panel_factor_async(int k, int method, int64_t n, int64_t jb, int64_t kw, double* re,
+                           double* im, int64_t ld, int64_t ps, int64_t* piv, int64_t* status_out,
+                           void* stream) {
+  if (bad_k(k)) return fail("k must be 2, 3 or 4");
+  if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
+  if (n < 0 || jb < 0 || kw < 0 || jb + kw > n) return fail("panel outside the matrix");
+  MPC_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = -1;
+  for (const void* p : {(const void*)re, (const void*)im, (const void*)piv, (const void*)status_out})
+    if (ptr_kind(p, &dev) != 2) return fail("mpc_panel_factor_async needs device pointers");
+  ck(cudaSetDevice(dev), "cudaSetDevice");
+  WsHolder w(k, n, st);
+  if (kw > 0)
+    table_for(k)->panel_rec(method == 3, mpc::View{re - jb, im - jb, ld, ps}, n, jb, kw, piv,
+                            w.ws, st);
+  ck(cudaMemcpyAsync(status_out, w.ws.status, sizeof(int64_t), cudaMemcpyDeviceToDevice, st),
+     "status copy");
+  ck(cudaGetLastError(), "kernel launch");
+  return 0;
   MPC_CATCH
 }
 

@@ -27,7 +27,6 @@ oracle-backed backend to exercise the same schedule with gloo.
 """
 
 from dataclasses import dataclass
-import time
 
 import numpy as np
 
@@ -113,9 +112,10 @@ class CudaBackend:
         return self.torch.empty(shape, dtype=dt, device=self.device)
 
     def panel_factor(self, V, n, jb, kw, piv):
+        # the C entry point takes the address of element (0, jb)
         return self._lib.check(self.L.mpc_panel_factor(
-            self.k, self.meth, n, jb, kw, self._p(V.re, V.off), self._p(V.im, V.off), V.ld, V.ps,
-            piv.data_ptr(), self._st()), "panel_factor")
+            self.k, self.meth, n, jb, kw, self._p(V.re, V.off + jb), self._p(V.im, V.off + jb),
+            V.ld, V.ps, piv.data_ptr(), self._st()), "panel_factor")
 
     def laswp(self, V, ncols, piv, r0, r1):
         if ncols <= 0:
@@ -144,6 +144,37 @@ class CudaBackend:
         buf_re.copy_(loc_re[:, jb:, lc:lc + kw])
         buf_im.copy_(loc_im[:, jb:, lc:lc + kw])
 
+    # --- asynchronous panel on a high-priority side stream (lookahead) ---
+    def side(self):
+        if not hasattr(self, "_side"):
+            self._side = self.torch.cuda.Stream(device=self.device, priority=-1)
+        return self._side
+
+    def side_context(self):
+        return self.torch.cuda.stream(self.side())
+
+    def side_wait_main(self):
+        self.side().wait_stream(self.torch.cuda.current_stream(self.device))
+
+    def main_wait_side(self):
+        self.torch.cuda.current_stream(self.device).wait_stream(self.side())
+
+    def panel_factor_meta(self, V, n, jb, kw, piv, meta):
+        """Enqueue the panel on the current stream; status -> meta[kw],
+        pivots -> meta[:kw] (device side, no host synchronisation)."""
+        self._lib.check(self.L.mpc_panel_factor_async(
+            self.k, self.meth, n, jb, kw, self._p(V.re, V.off + jb), self._p(V.im, V.off + jb),
+            V.ld, V.ps, piv.data_ptr(), meta[kw:].data_ptr(), self._st()), "panel_factor")
+        meta[:kw].copy_(piv[jb:jb + kw])
+
+
+class _NoStream:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
 
 def dist_getrf(backend, comm, lay, k, loc_re, loc_im, piv, lookahead=True):
     """Factor the distributed matrix in place.
@@ -161,26 +192,34 @@ def dist_getrf(backend, comm, lay, k, loc_re, loc_im, piv, lookahead=True):
     if nb == 0:
         return -1
 
+    asyncp = hasattr(backend, "panel_factor_meta")
+
     def panel_step(b):
-        """Owner side: factor panel b, pack it; returns (status, bufs)."""
+        """Factor panel b (owner) and start its broadcast; returns (bufs,
+        works).  With an async backend the panel and the broadcast run on
+        the side stream, so the caller's trailing update overlaps them."""
         jb, kw = b * K, lay.width(b)
         buf_re = backend.empty((k, n - jb, kw))
         buf_im = backend.empty((k, n - jb, kw))
         meta = backend.empty((kw + 1,), "i64")
-        if lay.owner(b) == lay.rank:
-            V = A.sub(0, lay.lcol[b] - jb)
-            st = backend.panel_factor(V, n, jb, kw, piv)
-            backend.pack_panel(loc_re, loc_im, lay, b, buf_re, buf_im)
-            meta[:kw].copy_(piv[jb:jb + kw])
-            meta[kw] = st
-        return buf_re, buf_im, meta
-
-    def bcast(b, bufs):
-        """Start the broadcast of panel b (async); returns the pending works."""
-        src = lay.owner(b)
-        buf_re, buf_im, meta = bufs
-        return [comm.broadcast(meta, src), comm.broadcast(buf_re, src),
-                comm.broadcast(buf_im, src)]
+        owner = lay.owner(b) == lay.rank
+        if asyncp:
+            backend.side_wait_main()
+        ctx = backend.side_context() if asyncp else _NoStream()
+        with ctx:
+            if owner:
+                V = A.sub(0, lay.lcol[b] - jb)
+                if asyncp:
+                    backend.panel_factor_meta(V, n, jb, kw, piv, meta)
+                else:
+                    st = backend.panel_factor(V, n, jb, kw, piv)
+                    meta[:kw].copy_(piv[jb:jb + kw])
+                    meta[kw] = st
+                backend.pack_panel(loc_re, loc_im, lay, b, buf_re, buf_im)
+            src = lay.owner(b)
+            works = [comm.broadcast(meta, src), comm.broadcast(buf_re, src),
+                     comm.broadcast(buf_im, src)]
+        return (buf_re, buf_im, meta), works
 
     def apply_panel(b, bufs, col_lo, col_hi):
         """LASWP + TRSM + trailing update for local columns [col_lo, col_hi)
@@ -210,6 +249,8 @@ def dist_getrf(backend, comm, lay, k, loc_re, loc_im, piv, lookahead=True):
             backend.gemm_sub(L11.sub(kw, 0), A.sub(jb, lo), A.sub(end, lo), n - end, kw, M)
 
     def check_status(b, bufs, works):
+        if asyncp:
+            backend.main_wait_side()
         for w in works:
             if w is not None:
                 w.wait()
@@ -221,27 +262,27 @@ def dist_getrf(backend, comm, lay, k, loc_re, loc_im, piv, lookahead=True):
         if st >= 0:
             raise SingularMatrixError(st)
 
-    bufs = panel_step(0)
-    works = bcast(0, bufs)
+    bufs, works = panel_step(0)
     for b in range(nb):
         check_status(b, bufs, works)
         nxt = b + 1 if b + 1 < nb else None
         if nxt is not None and lookahead and lay.owner(nxt) == lay.rank:
-            # update block nxt first, factor and ship panel nxt, then the rest
+            # update block nxt first, factor and ship panel nxt (side
+            # stream), then the rest of step b overlaps it
             c0 = lay.lcol[nxt]
             c1 = c0 + lay.width(nxt)
             apply_panel(b, bufs, c0, c1)
-            nbufs = panel_step(nxt)
-            nworks = bcast(nxt, nbufs)
+            nbufs, nworks = panel_step(nxt)
             apply_panel(b, bufs, 0, c0)
             apply_panel(b, bufs, c1, lay.ncols)
         else:
             apply_panel(b, bufs, 0, lay.ncols)
             if nxt is not None:
-                nbufs = panel_step(nxt)
-                nworks = bcast(nxt, nbufs)
+                nbufs, nworks = panel_step(nxt)
         if nxt is not None:
             bufs, works = nbufs, nworks
+    if asyncp:
+        backend.main_wait_side()
     return -1
 
 
