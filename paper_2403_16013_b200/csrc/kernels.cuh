@@ -86,9 +86,13 @@ MPC_DI void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N))
 
 // One CTA computes a BM x BN tile of C with (BM/TM) x (BN/TN) threads; each
 // thread owns a TM x TN strided micro-tile and NACC expansion chains per
-// element.  Inner dimension staged through shared memory in BK slabs with a
-// two-stage cp.async pipeline.  Smem layout per stage:
-//   As[NS][K][BM][BK], Bs[NS][K][BK][BN]   (limb planes kept separate)
+// element.  The inner dimension is staged through shared memory in BK slabs
+// with a two-stage cp.async pipeline.  Shared layout per stage keeps the
+// limbs of one element adjacent (one LDS.128 per DD operand):
+//   As[NS][BM][BK][K], Bs[NS][BK][BN][K].
+// Per slab: compute(kt) | wait(kt+1), barrier | Re+Im sums of kt+1 (3M) and
+// issue the loads of kt+2 | barrier -- two barriers per slab (one without
+// sums).
 template <int K, int MODE, int BM, int BN, int BK, int TM, int TN>
 struct GemmCfg {
   using MI = ModeInfo<MODE>;
@@ -98,6 +102,35 @@ struct GemmCfg {
   static constexpr size_t SMEM = sizeof(double) * 2 * (A_STAGE + B_STAGE);
 };
 
+// K consecutive doubles from shared memory (vectorised for even K)
+template <int K>
+MPC_DI Exp<K> lds_exp(const double* p) {
+  Exp<K> e;
+  if constexpr (K % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < K; c += 2) {
+      double2 v = *reinterpret_cast<const double2*>(p + c);
+      e.c[c] = v.x;
+      e.c[c + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < K; c++) e.c[c] = p[c];
+  }
+  return e;
+}
+template <int K>
+MPC_DI void sts_exp(double* p, const Exp<K>& e) {
+  if constexpr (K % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < K; c += 2)
+      *reinterpret_cast<double2*>(p + c) = make_double2(e.c[c], e.c[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < K; c++) p[c] = e.c[c];
+  }
+}
+
 template <int K, int MODE, int BM, int BN, int BK, int TM, int TN, int MINB>
 __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB)
     gemm_kernel(GemmArgs g) {
@@ -106,6 +139,7 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
   constexpr int SX = Cfg::SX, SY = Cfg::SY, NT = Cfg::NT;
   constexpr int NS = MI::NS, NL = MI::NLOAD, NACC = MI::NACC;
   constexpr int A_STAGE = Cfg::A_STAGE, B_STAGE = Cfg::B_STAGE;
+  constexpr int AE = NL * K * BM * BK, BE = NL * K * BK * BN;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + 2 * A_STAGE;
@@ -136,64 +170,73 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
       }
     }
 
+  // element e of a stage: tt (A) / cc (B) fastest -> coalesced global reads
   auto load_stage = [&](int st, int64_t t0) {
     double* as = As + st * A_STAGE;
     double* bs = Bs + st * B_STAGE;
-    constexpr int AE = NL * K * BM * BK;
-    for (int e = tid; e < AE; e += NT) {
-      int tt = e % BK;
-      int r = (e / BK) % BM;
-      int c = (e / (BK * BM)) % K;
-      int op = e / (BK * BM * K);
-      int64_t gi = row0 + r, gt = t0 + tt;
-      bool v = gi < g.m && gt < g.n;
+#pragma unroll
+    for (int i = 0; i < (AE + NT - 1) / NT; i++) {
+      const int e = tid + i * NT;
+      if (AE % NT != 0 && e >= AE) break;
+      const int tt = e % BK, r = (e / BK) % BM, c = (e / (BK * BM)) % K, op = e / (BK * BM * K);
+      const int64_t gi = row0 + r, gt = t0 + tt;
+      const bool v = gi < g.m && gt < g.n;
       const double* base = (op == 0) ? g.a.re : g.a.im;
       const double* src = v ? base + c * g.a.ps + gi * g.a.ld + gt : base;
-      cp_async8(as + ((op * K + c) * BM + r) * BK + tt, src, v);
+      cp_async8(as + ((op * BM + r) * BK + tt) * K + c, src, v);
     }
-    constexpr int BE = NL * K * BK * BN;
-    for (int e = tid; e < BE; e += NT) {
-      int cc = e % BN;
-      int tt = (e / BN) % BK;
-      int c = (e / (BN * BK)) % K;
-      int op = e / (BN * BK * K);
-      int64_t gt = t0 + tt, gj = col0 + cc;
-      bool v = gt < g.n && gj < g.l;
+#pragma unroll
+    for (int i = 0; i < (BE + NT - 1) / NT; i++) {
+      const int e = tid + i * NT;
+      if (BE % NT != 0 && e >= BE) break;
+      const int cc = e % BN, tt = (e / BN) % BK, c = (e / (BN * BK)) % K, op = e / (BN * BK * K);
+      const int64_t gt = t0 + tt, gj = col0 + cc;
+      const bool v = gt < g.n && gj < g.l;
       const double* base = (op == 0) ? g.b.re : g.b.im;
       const double* src = v ? base + c * g.b.ps + gt * g.b.ld + gj : base;
-      cp_async8(bs + ((op * K + c) * BK + tt) * BN + cc, src, v);
+      cp_async8(bs + ((op * BK + tt) * BN + cc) * K + c, src, v);
+    }
+  };
+
+  // slot 2 = Re + Im (mat_add_k / cmul_3m_core's exp_add), once per element
+  auto sums = [&](int st) {
+    if constexpr (MI::SUMS) {
+      double* as = As + st * A_STAGE;
+      double* bs = Bs + st * B_STAGE;
+      for (int e = tid; e < BM * BK; e += NT) {
+        Exp<K> x = lds_exp<K>(as + e * K);
+        Exp<K> y = lds_exp<K>(as + (BM * BK + e) * K);
+        sts_exp<K>(as + (2 * BM * BK + e) * K, exp_add(x, y));
+      }
+      for (int e = tid; e < BK * BN; e += NT) {
+        Exp<K> x = lds_exp<K>(bs + e * K);
+        Exp<K> y = lds_exp<K>(bs + (BK * BN + e) * K);
+        sts_exp<K>(bs + (2 * BK * BN + e) * K, exp_add(x, y));
+      }
     }
   };
 
   const int64_t nk = (g.n + BK - 1) / BK;
-  if (nk > 0) load_stage(0, 0);
-  cp_async_commit();
-  for (int64_t kt = 0; kt < nk; kt++) {
-    const int st = (int)(kt & 1);
-    if (kt + 1 < nk) {
-      load_stage(st ^ 1, (kt + 1) * BK);
+  if (nk > 0) {
+    load_stage(0, 0);
+    cp_async_commit();
+    if (nk > 1) {
+      load_stage(1, BK);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    double* as = As + st * A_STAGE;
-    double* bs = Bs + st * B_STAGE;
     if constexpr (MI::SUMS) {
-      // slot 2 = Re + Im (mat_add_k / cmul_3m_core's exp_add), once per element
-      for (int e = tid; e < BM * BK; e += NT) {
-        Exp<K> x = ldexp_<K>(as + e, BM * BK);
-        Exp<K> y = ldexp_<K>(as + K * BM * BK + e, BM * BK);
-        stexp_<K>(as + 2 * K * BM * BK + e, BM * BK, exp_add(x, y));
-      }
-      for (int e = tid; e < BK * BN; e += NT) {
-        Exp<K> x = ldexp_<K>(bs + e, BK * BN);
-        Exp<K> y = ldexp_<K>(bs + K * BK * BN + e, BK * BN);
-        stexp_<K>(bs + 2 * K * BK * BN + e, BK * BN, exp_add(x, y));
-      }
+      sums(0);
       __syncthreads();
     }
+  }
+  for (int64_t kt = 0; kt < nk; kt++) {
+    const int st = (int)(kt & 1);
+    const double* as = As + st * A_STAGE;
+    const double* bs = Bs + st * B_STAGE;
     const int tlen = (int)min((int64_t)BK, g.n - kt * BK);
 #pragma unroll
     for (int t = 0; t < BK; t++) {
@@ -203,10 +246,10 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
         for (int s = 0; s < NS; s++) {
 #pragma unroll
           for (int r = 0; r < TM; r++)
-            av[s][r] = ldexp_<K>(as + (s * K * BM + ty + r * SY) * BK + t, BM * BK);
+            av[s][r] = lds_exp<K>(as + ((s * BM + ty + r * SY) * BK + t) * K);
 #pragma unroll
           for (int c = 0; c < TN; c++)
-            bv[s][c] = ldexp_<K>(bs + (s * K * BK + t) * BN + tx + c * SX, BK * BN);
+            bv[s][c] = lds_exp<K>(bs + ((s * BK + t) * BN + tx + c * SX) * K);
         }
 #pragma unroll
         for (int r = 0; r < TM; r++)
@@ -235,7 +278,16 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
           }
       }
     }
-    __syncthreads();
+    if (kt + 1 < nk) {
+      cp_async_wait<0>();  // this thread's copies of slab kt+1 have landed
+      __syncthreads();     // ... everyone's, and everyone is done with slab kt
+      sums(st ^ 1);
+      if (kt + 2 < nk) {
+        load_stage(st, (kt + 2) * BK);  // refill the slab just consumed
+        cp_async_commit();
+      }
+      if constexpr (MI::SUMS) __syncthreads();
+    }
   }
   cp_async_wait<0>();
 
