@@ -738,9 +738,9 @@ struct Ops {
   // tile configurations (tuned per K)
   static constexpr int BM = (K == 2) ? 32 : 16;
   static constexpr int BN = (K == 2) ? 32 : 16;
-  // K=2: BK=16 measured best (cfg1 n=1024: 89.8% of FP64 peak vs 86.9% at
-  // BK=8; profiles/r1_gemm_variants.txt)
-  static constexpr int BK = (K == 2) ? 16 : 8;
+  // K=2: BK=8 with the limb-interleaved layout measured best (cfg1 n=4096:
+  // 93.2% of the FP64 peak; profiles/r1_gemm_variants.txt)
+  static constexpr int BK = 8;
   static constexpr int TM = (K == 2) ? 2 : 1;
   static constexpr int TN = (K == 2) ? 2 : 1;
 
@@ -775,7 +775,13 @@ struct Ops {
     double ops = (double)g.m * (double)g.l * (double)g.n * per_elem;
     if constexpr (K == 2) {
       switch (variant()) {
-        case 1: launch_cfg<MODE, 32, 32, 8, 2, 2, 2>(g, st, cls, ops); return;  // round-1 v0
+        case 1: launch_cfg<MODE, 32, 32, 16, 2, 2, 2>(g, st, cls, ops); return;  // BK=16
+        default: break;
+      }
+    } else {
+      switch (variant()) {
+        case 1: launch_cfg<MODE, 16, 16, 8, 1, 1, 2>(g, st, cls, ops); return;  // 2 CTA/SM
+        case 2: launch_cfg<MODE, 16, 8, 8, 1, 1, 3>(g, st, cls, ops); return;   // 128 thr
         default: break;
       }
     }
