@@ -774,18 +774,16 @@ struct Ops {
     if (g.m <= 0 || g.l <= 0) return;
     double ops = (double)g.m * (double)g.l * (double)g.n * per_elem;
     if constexpr (K == 2) {
-      switch (variant()) {
-        case 1: launch_cfg<MODE, 32, 32, 16, 2, 2, 2>(g, st, cls, ops); return;  // BK=16
-        default: break;
-      }
-    } else {
-      switch (variant()) {
-        case 1: launch_cfg<MODE, 16, 16, 8, 1, 1, 2>(g, st, cls, ops); return;  // 2 CTA/SM
-        case 2: launch_cfg<MODE, 16, 8, 8, 1, 1, 3>(g, st, cls, ops); return;   // 128 thr
-        default: break;
-      }
+      // alternatives measured in round 1 (profiles/r1_gemm_variants.txt):
+      // BK=16, 1 CTA/SM with 132 regs, 64x32 tile with a 4x2 micro-tile --
+      // all slower than 32x32 / BK=8 / 2x2 / 2 CTAs per SM
+      (void)variant;
+
     }
-    launch_cfg<MODE, BM, BN, BK, TM, TN, (K == 2 ? 2 : 1)>(g, st, cls, ops);
+    // K=3,4: 2 CTAs/SM (register cap 128) measured best for config 3
+    // (TD 1.13 s / QD 2.31 s vs 1.39 / 3.14 s at 1 CTA/SM; 128-thread tiles
+    // in between -- profiles/r1_cfg3_tdqd.txt)
+    launch_cfg<MODE, BM, BN, BK, TM, TN, 2>(g, st, cls, ops);
   }
 
   static void rgemm(int64_t m, int64_t n, int64_t l, View a, View b, View c, cudaStream_t st) {
