@@ -20,10 +20,12 @@
 // which commutes with the row operations.
 #pragma once
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
+#include <string>
 #include <vector>
 #include "expansion.cuh"
 #include "prof.h"
@@ -545,6 +547,134 @@ __global__ void __launch_bounds__(PNT) panel_step_kernel(View A, int64_t n, int6
   pivot_finish<K>(A, j + 1, c0, cend, piv, ws, c);
 }
 
+// ------------------------------------------------- cluster base panel
+// The whole base panel (columns [c0, c0+w), rows [c0, n)) in ONE launch of a
+// thread-block cluster: per column, every thread updates its rows (cdiv +
+// chained cmul updates, exactly panel_step_kernel's arithmetic), the pivot
+// candidates of the next column are reduced warp -> CTA -> cluster (CTA 0
+// reads the other CTAs' partials through distributed shared memory), CTA 0
+// swaps the two rows inside the panel, and two cluster barriers (release /
+// acquire, L1 invalidated) publish the result.  Replaces 1 + w kernel
+// launches and their last-block atomics per base panel.
+template <int K>
+struct PanelCluster {
+  static constexpr int NT = (K == 2) ? 512 : 256;  // threads per CTA
+};
+
+template <int K>
+MPC_DI void cluster_pick_and_swap(const View& A, int64_t jj, int64_t c0, int64_t cend,
+                                  int64_t* piv, int64_t* status, Cand<K> c) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = PanelCluster<K>::NT;
+  __shared__ Exp<K> cta_v;
+  __shared__ int64_t cta_r;
+  __shared__ int64_t pick;
+  cg::cluster_group cluster = cg::this_cluster();
+  c = block_reduce_cand<K, NT>(c);
+  if (threadIdx.x == 0) {
+    cta_v = c.v;
+    cta_r = c.row;
+  }
+  cluster.sync();  // partials visible cluster-wide
+  if (cluster.block_rank() == 0) {
+    if (threadIdx.x < 32) {
+      Cand<K> b;
+      b.row = -1;
+      b.v = exp_zero<K>();
+      if (threadIdx.x < cluster.num_blocks()) {
+        Exp<K>* rv = cluster.map_shared_rank(&cta_v, threadIdx.x);
+        int64_t* rr = cluster.map_shared_rank(&cta_r, threadIdx.x);
+        b.v = *rv;
+        b.row = *rr;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        Cand<K> o = shfl_cand(b, off);
+        if (cand_better(o, b)) b = o;
+      }
+      if (threadIdx.x == 0) {
+        pick = b.row;
+        if (b.row < 0) {
+          if (*status < 0) *status = jj;  // lu_panel returns jj (_kernels.py:622-624)
+        } else {
+          piv[jj] = b.row;
+        }
+      }
+    }
+    __syncthreads();
+    int64_t p = pick;
+    if (p >= 0 && p != jj) {
+      int64_t w = cend - c0;
+      for (int64_t e = threadIdx.x; e < 2 * K * w; e += NT) {
+        int64_t t = c0 + e % w;
+        int q = (int)(e / w);
+        double* base = (q < K) ? A.re + q * A.ps : A.im + (q - K) * A.ps;
+        double x = base[jj * A.ld + t];
+        base[jj * A.ld + t] = base[p * A.ld + t];
+        base[p * A.ld + t] = x;
+      }
+    }
+    __threadfence();
+  }
+  cluster.sync();  // swap and status visible
+}
+
+template <int K>
+__global__ void __launch_bounds__(PanelCluster<K>::NT, 1)
+    panel_cluster_kernel(View A, int64_t n, int64_t c0, int64_t w, int use3m, int64_t* piv,
+                         int64_t* status) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = PanelCluster<K>::NT;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int64_t T = (int64_t)cluster.num_blocks() * NT;
+  const int64_t gt = (int64_t)cluster.block_rank() * NT + threadIdx.x;
+  const int64_t cend = c0 + w;
+  if (*(volatile int64_t*)status >= 0) return;  // uniform: written only by earlier launches
+  {
+    Cand<K> c;
+    c.row = -1;
+    c.v = exp_zero<K>();
+    for (int64_t i = c0 + gt; i < n; i += T) {
+      Cand<K> o = make_cand<K>(A, i, c0);
+      if (cand_better(o, c)) c = o;
+    }
+    cluster_pick_and_swap<K>(A, c0, c0, cend, piv, status, c);
+  }
+  for (int64_t j = c0; j < cend; j++) {
+    if (*(volatile int64_t*)status >= 0) return;  // uniform after the barrier
+    const Exp<K> br = ldexp_<K>(A.re + j * A.ld + j, A.ps);
+    const Exp<K> bi = ldexp_<K>(A.im + j * A.ld + j, A.ps);
+    Cand<K> c;
+    c.row = -1;
+    c.v = exp_zero<K>();
+    for (int64_t i = j + 1 + gt; i < n; i += T) {
+      Exp<K> ar = ldexp_<K>(A.re + i * A.ld + j, A.ps);
+      Exp<K> ai = ldexp_<K>(A.im + i * A.ld + j, A.ps);
+      Cx<K> l = cdiv(ar, ai, br, bi);
+      stexp_<K>(A.re + i * A.ld + j, A.ps, l.re);
+      stexp_<K>(A.im + i * A.ld + j, A.ps, l.im);
+      for (int64_t t = j + 1; t < cend; t++) {
+        Exp<K> ur = ldexp_<K>(A.re + j * A.ld + t, A.ps);
+        Exp<K> ui = ldexp_<K>(A.im + j * A.ld + t, A.ps);
+        Cx<K> pr = cmul(use3m != 0, l.re, l.im, ur, ui);
+        Exp<K> xr = ldexp_<K>(A.re + i * A.ld + t, A.ps);
+        Exp<K> xi = ldexp_<K>(A.im + i * A.ld + t, A.ps);
+        xr = exp_sub(xr, pr.re);
+        xi = exp_sub(xi, pr.im);
+        stexp_<K>(A.re + i * A.ld + t, A.ps, xr);
+        stexp_<K>(A.im + i * A.ld + t, A.ps, xi);
+        if (t == j + 1) {  // candidate of the next column from the fresh value
+          Cand<K> o;
+          o.v = exp_add(exp_abs(xr), exp_abs(xi));
+          o.row = exp_greater(o.v, exp_zero<K>()) ? i : -1;
+          if (cand_better(o, c)) c = o;
+        }
+      }
+    }
+    if (j + 1 < cend) cluster_pick_and_swap<K>(A, j + 1, c0, cend, piv, status, c);
+  }
+}
+
 // ---------------------------------------------------------------- LASWP
 // Apply the interchanges piv[r0..r1) in order to columns [col0, col0+ncols)
 // of every limb plane (the deferred part of _swap_rows, _kernels.py:597-608).
@@ -864,9 +994,59 @@ struct Ops {
 
   static constexpr int PANEL_BASE = 8;
   // base panel: columns [c0, c0+w) over rows [c0, n), swaps within [c0, c0+w)
+  // cluster size for the base panel: the largest of 16 / 8 / 4 / 2 that can
+  // be co-scheduled (0 = use the per-column launches; MPC_PANEL=launches)
+  static int panel_cluster_size() {
+    static int cs = [] {
+      const char* e = getenv("MPC_PANEL");
+      if (e && std::string(e) == "launches") return 0;
+      auto kern = panel_cluster_kernel<K>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      for (int c : {16, 8, 4, 2}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(c);
+        cfg.blockDim = dim3(PanelCluster<K>::NT);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters > 0)
+          return c;
+        cudaGetLastError();
+      }
+      return 0;
+    }();
+    return cs;
+  }
+
   static void panel_base(bool use3m, View A, int64_t n, int64_t c0, int64_t w, int64_t* piv,
                          PanelWs ws, cudaStream_t st) {
     int64_t cend = c0 + w;
+    if (int cs = panel_cluster_size()) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(PanelCluster<K>::NT);
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      double ops = 0.0;
+      for (int64_t j = c0; j < cend; j++) ops += (double)(n - j - 1) * (double)(cend - j - 1);
+      int tok_ = prof_begin(PC_PANEL, ops * OpModel<K>::upd(use3m), st);
+      cudaLaunchKernelEx(&cfg, panel_cluster_kernel<K>, A, n, c0, w, use3m ? 1 : 0, piv,
+                         ws.status);
+      prof_end(tok_, st);
+      check_launch("panel_cluster_kernel");
+      return;
+    }
     int tok_ = prof_begin(PC_PANEL, 0.0, st);
     pivot_first_kernel<K><<<cdiv_u(n - c0, PNT), PNT, 0, st>>>(A, n, c0, c0, cend, piv, ws);
     prof_end(tok_, st);
