@@ -125,6 +125,36 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
 int mpc_getrs(int k, int method, int64_t n, const double* re, const double* im,
               const int64_t* piv, double* b_re, double* b_im, void* stream);
 
+/* ---- Ozaki scheme (ozaki.py:79-159): the alternative real kernel ---- */
+/* ozaki_split (ozaki.py:79-108) of a (rows x cols) planar operand into d
+ * binary64 parts (contiguous (d, rows, cols)) with grid units `scales`
+ * ((d, rows) for side 0 = "left", (d, cols) for side 1 = "right"). */
+int mpc_ozaki_split(int k, int64_t rows, int64_t cols, const double* a, int64_t lda,
+                    int64_t psa, int d, int width, int side, double* parts, double* scales,
+                    void* stream);
+/* acc_plane (_kernels.py:502-517): C += P by ordered two-sum insertion. */
+int mpc_acc_plane(int k, int64_t rows, int64_t cols, double* c, int64_t ldc, int64_t psc,
+                  const double* p, int64_t ldp, void* stream);
+/* The f64_gemm seam (ozaki.py:127-142): Z = X Y in binary64 (cuBLAS DGEMM;
+ * exact, hence bit-identical to np.matmul, for Ozaki parts). */
+int mpc_f64_gemm(int64_t m, int64_t n, int64_t l, const double* x, int64_t ldx,
+                 const double* y, int64_t ldy, double* z, int64_t ldz, void* stream);
+/* rgemm_ozaki (ozaki.py:124-159); split_bits 0 = the default width. */
+int mpc_rgemm_ozaki(int k, int64_t m, int64_t n, int64_t l, const double* a, int64_t lda,
+                    int64_t psa, const double* b, int64_t ldb, int64_t psb, double* c,
+                    int64_t ldc, int64_t psc, int d, int split_bits, void* stream);
+/* cgemm_3m / cgemm_4m with real_kernel="ozaki" (cmatrix.py:128-169);
+ * epilogue as mpc_cgemm. */
+int mpc_cgemm_ozaki(int k, int method, int64_t m, int64_t n, int64_t l,
+                    const double* a_re, const double* a_im, int64_t lda, int64_t psa,
+                    const double* b_re, const double* b_im, int64_t ldb, int64_t psb,
+                    double* c_re, double* c_im, int64_t ldc, int64_t psc, int d, int split_bits,
+                    int epilogue, void* stream);
+/* lu_blocked with kc.real_kernel == "ozaki" (lu.py:129-163); piv must hold
+ * 0..n-1 on entry (lu.py:134).  Synchronous. */
+int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, double* im,
+                        int64_t* piv, int d, int split_bits, void* stream);
+
 /* ---- measurement hooks (bench.py) ---- */
 /* Per-launch CUDA-event timing of the kernel classes whose bit is set in
  * `mask` (bit c = class c below; 0 disables).  Clears previous records. */

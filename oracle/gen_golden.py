@@ -341,6 +341,50 @@ def gen_cfg3(n=2048, K=128):
                 json.dump(res, fh)
 
 
+def gen_ozaki():
+    """ozaki.py: split parts/scales, rgemm_ozaki, cgemm and lu_blocked with
+    real_kernel="ozaki" -- the f1 row's golden vectors."""
+    from mpclu import ozaki_split, rgemm_ozaki
+
+    rng = np.random.default_rng(20240802)
+    out = {}
+
+    def rmat(r, c, k):
+        return mpclu.rmatrix.random_matrix(r, c, k, rng).data
+
+    for k in (2, 3, 4):
+        A = rmat(12, 10, k)
+        B = rmat(10, 9, k)
+        out[f"oz_A_k{k}"], out[f"oz_B_k{k}"] = A, B
+        for d in (1, 3, 6):
+            sa = ozaki_split(RealMatrix(A), d, "left")
+            sb = ozaki_split(RealMatrix(B), d, "right")
+            out[f"oz_sa_parts_k{k}_d{d}"] = np.array(sa.parts)
+            out[f"oz_sa_scales_k{k}_d{d}"] = np.array(sa.scales)
+            out[f"oz_sb_parts_k{k}_d{d}"] = np.array(sb.parts)
+            out[f"oz_sb_scales_k{k}_d{d}"] = np.array(sb.scales)
+        for d in ({2: (5, 6), 3: (7, 8), 4: (11, 12)}[k]):
+            out[f"oz_C_k{k}_d{d}"] = rgemm_ozaki(RealMatrix(A), RealMatrix(B), d).data
+        out[f"oz_C_k{k}_d4_sb12"] = rgemm_ozaki(RealMatrix(A), RealMatrix(B), 4, split_bits=12).data
+        Ar, Ai, Br, Bi = rmat(13, 11, k), rmat(13, 11, k), rmat(11, 7, k), rmat(11, 7, k)
+        out[f"ozc_Ar_k{k}"], out[f"ozc_Ai_k{k}"] = Ar, Ai
+        out[f"ozc_Br_k{k}"], out[f"ozc_Bi_k{k}"] = Br, Bi
+        for meth in ("3m", "4m"):
+            C = cgemm(pc(Ar, Ai), pc(Br, Bi), KernelChoice(method=meth, real_kernel="ozaki"))
+            out[f"ozc_{meth}_k{k}"] = np.array([C.re_plane.data, C.im_plane.data])
+        n = 30
+        re, im = rmat(n, n, k), rmat(n, n, k)
+        re[0] -= 0.5
+        out[f"ozlu_re_k{k}"], out[f"ozlu_im_k{k}"] = re, im
+        for meth in ("3m", "4m"):
+            f = lu_blocked(pc(re, im), 8, kc=KernelChoice(method=meth, real_kernel="ozaki"))
+            out[f"ozlu_{meth}_k{k}"] = np.array([f.packed.re_plane.data, f.packed.im_plane.data])
+            out[f"ozlu_{meth}_k{k}_piv"] = f.pivots
+    path = os.path.join(GOLD, "ozaki.npz")
+    np.savez_compressed(path, **out)
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
 if __name__ == "__main__":
     os.makedirs(GOLD, exist_ok=True)
     for what in sys.argv[1:]:
@@ -348,4 +392,4 @@ if __name__ == "__main__":
             gen_cfg3(n=512, K=128)
             continue
         {"small": gen_small, "cfg0": gen_cfg0, "cfg1": gen_cfg1, "cfg2": gen_cfg2,
-         "cfg3": gen_cfg3}[what]()
+         "cfg3": gen_cfg3, "ozaki": gen_ozaki}[what]()

@@ -33,6 +33,7 @@ from .lu import (
     solve,
     trsm_unit_lower,
 )
+from .ozaki import SplitStack, ozaki_split, rgemm_ozaki, split_exactness_bound
 from .expansion import PRECISIONS, PRECISION_BITS, REFERENCE_K, eps_for, digits_for
 
 __version__ = "0.1.0"

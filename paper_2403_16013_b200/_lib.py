@@ -33,6 +33,14 @@ _SIGS = {
     "mpc_laswp": (_i, [_i, _i64, _p, _p, _i64, _i64, _p, _i64, _i64, _p]),
     "mpc_getrf": (_i64, [_i, _i, _i64, _i64, _p, _p, _p, _p]),
     "mpc_getrs": (_i, [_i, _i, _i64, _p, _p, _p, _p, _p, _p]),
+    "mpc_ozaki_split": (_i, [_i, _i64, _i64, _p, _i64, _i64, _i, _i, _i, _p, _p, _p]),
+    "mpc_acc_plane": (_i, [_i, _i64, _i64, _p, _i64, _i64, _p, _i64, _p]),
+    "mpc_f64_gemm": (_i, [_i64, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, _p]),
+    "mpc_rgemm_ozaki": (_i, [_i, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _i64, _p, _i64,
+                             _i64, _i, _i, _p]),
+    "mpc_cgemm_ozaki": (_i, [_i, _i, _i64, _i64, _i64, _p, _p, _i64, _i64, _p, _p, _i64, _i64,
+                             _p, _p, _i64, _i64, _i, _i, _i, _p]),
+    "mpc_getrf_ozaki": (_i64, [_i, _i, _i64, _i64, _p, _p, _p, _i, _i, _p]),
     "mpc_prof_enable": (None, [_i]),
     "mpc_prof_summary": (_i, [_p, _p, _p, _i]),
     "mpc_launch_count": (ctypes.c_longlong, []),

@@ -22,8 +22,8 @@ LIBDIR = os.path.join(HERE, "lib")
 OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libmpcb200.so")
 
-SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "abi.cu"]
-HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h"]
+SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "abi.cu", "ozaki.cu"]
+HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h", "abi_util.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -47,7 +47,7 @@ def _stale(out, deps):
 def _compile(src, verbose):
     obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
-    if src == "abi.cu":
+    if src in ("abi.cu", "ozaki.cu"):
         deps.append(os.path.join(os.path.dirname(HERE), "include", "mpc_b200.h"))
     if not _stale(obj, deps):
         return obj, ""
@@ -69,8 +69,9 @@ def build(verbose=False, force=False):
     objs = [o for o, _ in results]
     logs = "".join(l for _, l in results)
     if _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt",
-                                                                 "-lpthread", "-ldl"]
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + [
+            "-lcudart_static", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-lrt",
+            "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -184,17 +184,30 @@ def _cgemm(A, B, kc, method):
     _check_mm(A.re_plane, B.re_plane)
     kc.validate()
     check_threads(kc.threads)
-    if kc.real_kernel in ("strassen", "ozaki"):
-        raise NotImplementedError(
-            f"real_kernel={kc.real_kernel!r} is not on the B200 path yet (DESIGN.md, next rows)")
+    if kc.real_kernel == "strassen":
+        raise NotImplementedError("strassen is outside the B200 hot path (see DESIGN.md)")
     _check_k(A.k)
-    _kernel_calls[kc.real_kernel] += 3 if method == "3m" else 4
     k, m, n = A.re_plane.data.shape
     l = B.cols
     Cre, Cim = np.empty((k, m, l)), np.empty((k, m, l))
+    L = _lib.lib()
+    meth = 3 if method == "3m" else 4
+    if kc.real_kernel == "ozaki":
+        # cmatrix.py:128-135 -> rgemm_ozaki per real product, composed on device
+        from .ozaki import _resolve_width
+
+        _resolve_width(k, n, kc.split_bits)  # the reference's budget errors
+        _kernel_calls["ozaki"] += 3 if method == "3m" else 4
+        if m * l:
+            _lib.check(L.mpc_cgemm_ozaki(
+                k, meth, m, n, l, _lib.ptr(A.re_plane.data), _lib.ptr(A.im_plane.data), n, m * n,
+                _lib.ptr(B.re_plane.data), _lib.ptr(B.im_plane.data), l, n * l, _lib.ptr(Cre),
+                _lib.ptr(Cim), l, m * l, kc.splits_for(k),
+                int(kc.split_bits) if kc.split_bits is not None else 0, 0, None), "cgemm_ozaki")
+        return PlanarComplexMatrix(RealMatrix(Cre), RealMatrix(Cim))
+    _kernel_calls[kc.real_kernel] += 3 if method == "3m" else 4
     if m * l:
-        L = _lib.lib()
-        _lib.check(L.mpc_cgemm(k, 3 if method == "3m" else 4, m, n, l,
+        _lib.check(L.mpc_cgemm(k, meth, m, n, l,
                                _lib.ptr(A.re_plane.data), _lib.ptr(A.im_plane.data), n, m * n,
                                _lib.ptr(B.re_plane.data), _lib.ptr(B.im_plane.data), l, n * l,
                                _lib.ptr(Cre), _lib.ptr(Cim), l, m * l, 0, None), "cgemm")

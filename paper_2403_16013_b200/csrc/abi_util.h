@@ -1,0 +1,166 @@
+// abi_util.h -- shared helpers of the C-ABI translation units (abi.cu,
+// ozaki.cu): error reporting, pointer classification, host staging, the
+// pivot-reduction workspace.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/mpc_b200.h"
+#include "kernels.cuh"
+#include "ops.h"
+
+namespace mpcabi {
+
+extern thread_local std::string g_err;
+
+inline int fail(const std::string& msg) {
+  g_err = msg;
+  return MPC_ERR;
+}
+
+struct CudaError {
+  std::string what;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+inline const mpc::OpsTable* table_for(int k) {
+  switch (k) {
+    case 2: return mpc::ops_k2();
+    case 3: return mpc::ops_k3();
+    case 4: return mpc::ops_k4();
+    default: return nullptr;
+  }
+}
+
+// 0: null, 1: host, 2: device
+inline int ptr_kind(const void* p, int* device) {
+  if (p == nullptr) return 0;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    if (device) *device = a.device;
+    return 2;
+  }
+  return 1;
+}
+
+inline int64_t extent(int k, int64_t rows, int64_t cols, int64_t ld, int64_t ps) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return (int64_t)(k - 1) * ps + (rows - 1) * ld + cols;
+}
+
+// Maps every pointer of one call to device memory.  All-device calls pass
+// through untouched; all-host calls are staged (H2D before, D2H after, then
+// the stream is synchronised).
+class Stager {
+ public:
+  explicit Stager(cudaStream_t st) : st_(st) {}
+  ~Stager() {
+    for (auto& r : regs_)
+      if (r.dev) cudaFreeAsync(r.dev, st_);
+  }
+  bool classify(std::initializer_list<const void*> ptrs) {
+    int kinds = 0;
+    int dev = -1;
+    for (const void* p : ptrs) {
+      int d = -1;
+      int kd = ptr_kind(p, &d);
+      if (kd == 0) continue;
+      kinds |= (1 << kd);
+      if (kd == 2) dev = d;
+    }
+    if (kinds == ((1 << 1) | (1 << 2))) {
+      g_err = "mixed host and device pointers in one call";
+      return false;
+    }
+    host_ = (kinds == (1 << 1));
+    if (!host_ && dev >= 0) ck(cudaSetDevice(dev), "cudaSetDevice");
+    return true;
+  }
+  bool host() const { return host_; }
+  template <typename T>
+  T* map(T* p, int64_t nelem, bool in, bool out) {
+    if (!host_ || p == nullptr || nelem <= 0) return p;
+    Region r{(void*)p, (size_t)nelem * sizeof(T), out, nullptr};
+    ck(cudaMallocAsync(&r.dev, r.bytes, st_), "cudaMallocAsync");
+    regs_.push_back(r);
+    if (in) ck(cudaMemcpyAsync(r.dev, p, r.bytes, cudaMemcpyHostToDevice, st_), "H2D");
+    return (T*)r.dev;
+  }
+  void finish() {
+    if (host_) {
+      for (auto& r : regs_)
+        if (r.out) ck(cudaMemcpyAsync(r.host, r.dev, r.bytes, cudaMemcpyDeviceToHost, st_), "D2H");
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    if (host_) ck(cudaStreamSynchronize(st_), "cudaStreamSynchronize");
+  }
+
+ private:
+  struct Region {
+    void* host;
+    size_t bytes;
+    bool out;
+    void* dev;
+  };
+  cudaStream_t st_;
+  bool host_ = false;
+  std::vector<Region> regs_;
+};
+
+// pivot-reduction workspace + status word, stream ordered
+struct WsHolder {
+  mpc::PanelWs ws{};
+  cudaStream_t st;
+  void* mem = nullptr;
+  WsHolder(int k, int64_t n, cudaStream_t s) : st(s) {
+    int64_t nb = (n + mpc::PNT - 1) / mpc::PNT + 1;
+    size_t bytes = sizeof(double) * nb * k + sizeof(int64_t) * nb + 64;
+    ck(cudaMallocAsync(&mem, bytes, st), "cudaMallocAsync(ws)");
+    char* b = (char*)mem;
+    ws.status = (int64_t*)b;
+    ws.counter = (unsigned*)(b + 16);
+    ws.prow = (int64_t*)(b + 64);
+    ws.pv = (double*)(b + 64 + sizeof(int64_t) * nb);
+    ck(cudaMemsetAsync(ws.status, 0xFF, sizeof(int64_t), st), "memset status");
+    ck(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), st), "memset counter");
+  }
+  int64_t read_status() {
+    int64_t h = -1;
+    ck(cudaMemcpyAsync(&h, ws.status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H status");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    return h;
+  }
+  ~WsHolder() {
+    if (mem) cudaFreeAsync(mem, st);
+  }
+};
+
+inline bool bad_k(int k) { return table_for(k) == nullptr; }
+inline bool bad_method(int m) { return m != 3 && m != 4; }
+
+#define MPC_TRY try {
+#define MPC_CATCH                                                          \
+  }                                                                        \
+  catch (const mpcabi::CudaError& e) {                                     \
+    return mpcabi::fail(e.what);                                           \
+  }                                                                        \
+  catch (const mpc::LaunchError& e) {                                      \
+    return mpcabi::fail(std::string("launch failed: ") + e.what + ": " +   \
+                        cudaGetErrorString(cudaGetLastError()));           \
+  }                                                                        \
+  catch (const std::exception& e) {                                        \
+    return mpcabi::fail(e.what());                                         \
+  }
+
+}  // namespace mpcabi

@@ -295,9 +295,12 @@ class TorchComm:
 
 
 def lu_blocked_distributed(re, im, K, method="3m", lookahead=True):
-    """Factor a (k, n, n) host matrix over all ranks of the default process
-    group (one CUDA device per rank, NCCL); returns (packed_re, packed_im,
-    pivots) on rank 0 (None elsewhere)."""
+    """Public multi-GPU entry point: factor a (k, n, n) host matrix over all
+    ranks of the default process group (one CUDA device per rank, NCCL).
+    Every rank passes the same host arrays (each copies only its own block
+    columns to its device); rank 0 receives (packed_re, packed_im, pivots) as
+    host arrays, the other ranks None.  Raises SingularMatrixError on every
+    rank like lu_blocked."""
     import torch
     import torch.distributed as dist
 
@@ -310,17 +313,33 @@ def lu_blocked_distributed(re, im, K, method="3m", lookahead=True):
     piv = torch.arange(n, dtype=torch.int64, device=dev)
     be = CudaBackend(k, method, dev)
     dist_getrf(be, TorchComm(dist), lay, k, loc_re, loc_im, piv, lookahead)
-    # gather to rank 0
-    lr, li = loc_re.cpu().numpy(), loc_im.cpu().numpy()
-    objs = [None] * world
-    dist.all_gather_object(objs, (rank, lr, li))
+    return gather_factors(lay, loc_re, loc_im, piv, re.shape)
+
+
+def gather_factors(lay, loc_re, loc_im, piv, shape):
+    """NCCL gather of every rank's block columns to rank 0 (padded to the
+    widest rank), then one D2H copy on rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    k, n, _ = shape
+    world, rank = lay.world, lay.rank
+    wmax = max(Layout(n, lay.K, world, r).ncols for r in range(world))
+    out = []
+    for t in (loc_re, loc_im):
+        pad = torch.zeros((k, n, wmax), dtype=t.dtype, device=t.device)
+        pad[:, :, :lay.ncols].copy_(t)
+        bufs = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
+        dist.gather(pad, bufs, dst=0)
+        out.append(bufs)
     if rank != 0:
         return None
-    fr, fi = np.empty_like(re), np.empty_like(im)
-    for r, a, b in objs:
-        L = Layout(n, K, world, r)
-        L.gather_into(fr, a)
-        L.gather_into(fi, b)
+    fr = np.empty(shape)
+    fi = np.empty(shape)
+    for r in range(world):
+        L = Layout(n, lay.K, world, r)
+        L.gather_into(fr, out[0][r][:, :, :L.ncols].cpu().numpy())
+        L.gather_into(fi, out[1][r][:, :, :L.ncols].cpu().numpy())
     return fr, fi, piv.cpu().numpy()
 
 
@@ -356,6 +375,12 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
         step()
     torch.cuda.synchronize()
     dist.barrier()
+    clocks = None
+    if rank == 0:
+        from bench import ClockSampler
+
+        clocks = ClockSampler(dev.index)
+        clocks.start()
     l0 = _lib.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -368,6 +393,30 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dist.barrier()
     ms_step = float(ms.item()) / args.steps
+    launches = int(_lib.launch_count() - l0)
+    clk = clocks.stop() if clocks else None
+    # e2e: the public multi-GPU API from host arrays (H2D scatter, factor,
+    # NCCL gather, D2H on rank 0), device-timed on every rank, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        res = lu_blocked_distributed(re0, im0, K, args.method)
+        a1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([a0.elapsed_time(a1)], device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        same = None
+        if rank == 0:
+            same = bool(np.array_equal(res[2], piv.cpu().numpy()))
+        e2e = {"value": 8.0 * n ** 3 / 3.0 / (float(te.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(re0.nbytes + im0.nbytes),
+               "d2h_bytes_per_step": int(re0.nbytes + im0.nbytes + 8 * n),
+               "ms_per_step": float(te.item()), "steps": 1, "pivots_match_device_run": same,
+               "api": "paper_2403_16013_b200.dist.lu_blocked_distributed"}
     pv = [torch.empty_like(piv) for _ in range(world)]
     dist.all_gather(pv, piv)
     consistent = all(bool(torch.equal(pv[0], p)) for p in pv)
@@ -380,8 +429,8 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
                "config": {"workload": workload, "n": n, "K": K, "k": k, "method": args.method,
                           "parallelism": f"1-D block-column-cyclic over {world} GPUs, NCCL "
                                          "panel+pivot broadcast, lookahead 1"},
-               "pivots_consistent_across_ranks": consistent,
-               "gpu_launches": int(_lib.launch_count() - l0),
+               "pivots_consistent_across_ranks": consistent, "clocks": clk, "e2e": e2e,
+               "gpu_launches": launches, "roofline": None, "cpu_baseline": None,
                "timing": "CUDA events per rank, max over ranks"}
         print(json.dumps(out), flush=True)
     dist.barrier()

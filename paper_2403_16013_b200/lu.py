@@ -101,15 +101,22 @@ class LUFactors:
         return U
 
 
-def _factor(A, K, method):
+def _factor(A, K, method, kc=None):
     """lu._factor (lu.py:129-163) as one device call."""
     n, k = A.rows, A.k
     _check_k(k)
     re = A.re_plane.data.copy()
     im = A.im_plane.data.copy()
     piv = np.arange(n, dtype=np.int64)
-    if n:
-        st = _lib.check(_lib.lib().mpc_getrf(k, 3 if method == "3m" else 4, n, K, _lib.ptr(re),
+    meth = 3 if method == "3m" else 4
+    if n and kc is not None and kc.real_kernel == "ozaki":
+        st = _lib.check(_lib.lib().mpc_getrf_ozaki(
+            k, meth, n, K, _lib.ptr(re), _lib.ptr(im), _lib.ptr(piv), kc.splits_for(k),
+            int(kc.split_bits) if kc.split_bits is not None else 0, None), "getrf_ozaki")
+        if st >= 0:
+            raise SingularMatrixError(int(st))
+    elif n:
+        st = _lib.check(_lib.lib().mpc_getrf(k, meth, n, K, _lib.ptr(re),
                                              _lib.ptr(im), _lib.ptr(piv), None), "getrf")
         if st >= 0:
             raise SingularMatrixError(int(st))
@@ -137,10 +144,9 @@ def lu_blocked(A, K, kc=None, threads=1):
         kc = KernelChoice()
     kc = kc.validate().with_threads(threads)
     check_threads(threads)
-    if kc.real_kernel in ("strassen", "ozaki"):
-        raise NotImplementedError(
-            f"real_kernel={kc.real_kernel!r} is not on the B200 path yet (DESIGN.md, next rows)")
-    return _factor(A, K, kc.method)
+    if kc.real_kernel == "strassen":
+        raise NotImplementedError("strassen is outside the B200 hot path (see DESIGN.md)")
+    return _factor(A, K, kc.method, kc)
 
 
 def trsm_unit_lower(L11, A12, method="3m", threads=1):

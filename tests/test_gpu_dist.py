@@ -90,3 +90,37 @@ def test_dist_cuda_backend_bitwise(world, backend, case):
         p.join(timeout=600)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) == "ok"
+
+
+def _public_worker(port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_16013_b200 as pkg
+    from paper_2403_16013_b200 import problems
+    from paper_2403_16013_b200.dist import lu_blocked_distributed
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        re, im = problems.lu_matrix(200, 2, 5)
+        fr, fi, piv = lu_blocked_distributed(re, im, 48, "3m")
+        f = pkg.lu_blocked(pkg.PlanarComplexMatrix(pkg.RealMatrix(re), pkg.RealMatrix(im)), 48)
+        ok = (np.array_equal(piv, f.pivots) and fr.tobytes() == f.packed.re_plane.data.tobytes()
+              and fi.tobytes() == f.packed.im_plane.data.tobytes())
+        q.put("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_public_distributed_api_nccl():
+    """lu_blocked_distributed (scatter from host, NCCL gather to rank 0)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_public_worker, args=(_free_port(), q))
+    p.start()
+    p.join(timeout=600)
+    assert p.exitcode == 0
+    assert q.get(timeout=5) == "ok"
