@@ -149,7 +149,16 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
   if (g.status != nullptr && *g.status >= 0) return;
   const int tid = threadIdx.x;
   const int tx = tid % SX, ty = tid / SX;
-  const int64_t row0 = (int64_t)blockIdx.y * BM, col0 = (int64_t)blockIdx.x * BN;
+  // grouped raster: G consecutive row tiles sweep the column tiles together,
+  // so one B column panel is reused from L2 by G CTAs in flight
+  constexpr int64_t G = 8;
+  const int64_t tiles_m = (g.m + BM - 1) / BM, tiles_n = (g.l + BN - 1) / BN;
+  const int64_t bid = blockIdx.x;
+  const int64_t grp = bid / (G * tiles_n);
+  const int64_t first_m = grp * G;
+  const int64_t gsz = min(tiles_m - first_m, G);
+  const int64_t in_grp = bid - grp * G * tiles_n;
+  const int64_t row0 = (first_m + in_grp % gsz) * BM, col0 = (in_grp / gsz) * BN;
 
   // accumulators
   Exp<K> acc[TM][TN][NACC];
@@ -558,7 +567,8 @@ __global__ void __launch_bounds__(PNT) panel_step_kernel(View A, int64_t n, int6
 // launches and their last-block atomics per base panel.
 template <int K>
 struct PanelCluster {
-  static constexpr int NT = (K == 2) ? 512 : 256;  // threads per CTA
+  static constexpr int NT = 256;                    // threads per CTA
+  static constexpr int WMAX = 8;                    // base panel width
 };
 
 template <int K>
@@ -640,35 +650,55 @@ __global__ void __launch_bounds__(PanelCluster<K>::NT, 1)
     }
     cluster_pick_and_swap<K>(A, c0, c0, cend, piv, status, c);
   }
+  constexpr int W = PanelCluster<K>::WMAX;
   for (int64_t j = c0; j < cend; j++) {
     if (*(volatile int64_t*)status >= 0) return;  // uniform after the barrier
+    // the pivot row (a_jj and a_jt, t in (j, cend)) in registers, one round trip
     const Exp<K> br = ldexp_<K>(A.re + j * A.ld + j, A.ps);
     const Exp<K> bi = ldexp_<K>(A.im + j * A.ld + j, A.ps);
+    Exp<K> ur[W], ui[W];
+#pragma unroll
+    for (int q = 0; q < W; q++) {
+      int64_t t = j + 1 + q;
+      if (t < cend) {
+        ur[q] = ldexp_<K>(A.re + j * A.ld + t, A.ps);
+        ui[q] = ldexp_<K>(A.im + j * A.ld + t, A.ps);
+      }
+    }
     Cand<K> c;
     c.row = -1;
     c.v = exp_zero<K>();
     for (int64_t i = j + 1 + gt; i < n; i += T) {
       Exp<K> ar = ldexp_<K>(A.re + i * A.ld + j, A.ps);
       Exp<K> ai = ldexp_<K>(A.im + i * A.ld + j, A.ps);
+      Exp<K> xr[W], xi[W];
+#pragma unroll
+      for (int q = 0; q < W; q++) {
+        int64_t t = j + 1 + q;
+        if (t < cend) {
+          xr[q] = ldexp_<K>(A.re + i * A.ld + t, A.ps);
+          xi[q] = ldexp_<K>(A.im + i * A.ld + t, A.ps);
+        }
+      }
       Cx<K> l = cdiv(ar, ai, br, bi);
       stexp_<K>(A.re + i * A.ld + j, A.ps, l.re);
       stexp_<K>(A.im + i * A.ld + j, A.ps, l.im);
-      for (int64_t t = j + 1; t < cend; t++) {
-        Exp<K> ur = ldexp_<K>(A.re + j * A.ld + t, A.ps);
-        Exp<K> ui = ldexp_<K>(A.im + j * A.ld + t, A.ps);
-        Cx<K> pr = cmul(use3m != 0, l.re, l.im, ur, ui);
-        Exp<K> xr = ldexp_<K>(A.re + i * A.ld + t, A.ps);
-        Exp<K> xi = ldexp_<K>(A.im + i * A.ld + t, A.ps);
-        xr = exp_sub(xr, pr.re);
-        xi = exp_sub(xi, pr.im);
-        stexp_<K>(A.re + i * A.ld + t, A.ps, xr);
-        stexp_<K>(A.im + i * A.ld + t, A.ps, xi);
-        if (t == j + 1) {  // candidate of the next column from the fresh value
-          Cand<K> o;
-          o.v = exp_add(exp_abs(xr), exp_abs(xi));
-          o.row = exp_greater(o.v, exp_zero<K>()) ? i : -1;
-          if (cand_better(o, c)) c = o;
+#pragma unroll
+      for (int q = 0; q < W; q++) {
+        int64_t t = j + 1 + q;
+        if (t < cend) {  // independent across q: a_it -= cmul(l, a_jt)
+          Cx<K> pr = cmul(use3m != 0, l.re, l.im, ur[q], ui[q]);
+          xr[q] = exp_sub(xr[q], pr.re);
+          xi[q] = exp_sub(xi[q], pr.im);
+          stexp_<K>(A.re + i * A.ld + t, A.ps, xr[q]);
+          stexp_<K>(A.im + i * A.ld + t, A.ps, xi[q]);
         }
+      }
+      if (j + 1 < cend) {  // candidate of the next column from the fresh value
+        Cand<K> o;
+        o.v = exp_add(exp_abs(xr[0]), exp_abs(xi[0]));
+        o.row = exp_greater(o.v, exp_zero<K>()) ? i : -1;
+        if (cand_better(o, c)) c = o;
       }
     }
     if (j + 1 < cend) cluster_pick_and_swap<K>(A, j + 1, c0, cend, piv, status, c);
@@ -883,7 +913,7 @@ struct Ops {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
       attr_set = true;
     }
-    dim3 grid(cdiv_u(g.l, BN_), cdiv_u(g.m, BM_));
+    dim3 grid((unsigned)((int64_t)cdiv_u(g.l, BN_) * (int64_t)cdiv_u(g.m, BM_)));
     int tok_ = prof_begin(cls, ops, st);
     kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(g);
     prof_end(tok_, st);
@@ -992,7 +1022,7 @@ struct Ops {
     trsm(use3m, kb - h, M, L.sub(h, h), X.sub(h, 0), st, status);
   }
 
-  static constexpr int PANEL_BASE = 8;
+  static constexpr int PANEL_BASE = PanelCluster<K>::WMAX;
   // base panel: columns [c0, c0+w) over rows [c0, n), swaps within [c0, c0+w)
   // cluster size for the base panel: the largest of 16 / 8 / 4 / 2 that can
   // be co-scheduled (0 = use the per-column launches; MPC_PANEL=launches)
@@ -1026,7 +1056,10 @@ struct Ops {
   static void panel_base(bool use3m, View A, int64_t n, int64_t c0, int64_t w, int64_t* piv,
                          PanelWs ws, cudaStream_t st) {
     int64_t cend = c0 + w;
-    if (int cs = panel_cluster_size()) {
+    if (int csmax = panel_cluster_size()) {
+      // smallest power-of-two cluster giving every thread at most one row
+      int cs = 1;
+      while (cs < csmax && (int64_t)cs * PanelCluster<K>::NT < n - c0) cs *= 2;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs);
       cfg.blockDim = dim3(PanelCluster<K>::NT);
