@@ -22,7 +22,7 @@ LIBDIR = os.path.join(HERE, "lib")
 OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libmpcb200.so")
 
-SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "abi.cu", "ozaki.cu"]
+SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "abi.cu", "ozaki.cu", "ozaki_tc.cu"]
 HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h", "abi_util.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -47,6 +47,8 @@ def _stale(out, deps):
 def _compile(src, verbose):
     obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
+    if src in ("ozaki.cu", "ozaki_tc.cu"):
+        deps.append(os.path.join(CSRC, "ozaki_tc.h"))
     if src in ("abi.cu", "ozaki.cu"):
         deps.append(os.path.join(os.path.dirname(HERE), "include", "mpc_b200.h"))
     if not _stale(obj, deps):

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "abi_util.h"
+#include "ozaki_tc.h"
 #include "prof.h"
 
 using namespace mpcabi;
@@ -245,23 +246,30 @@ int resolve_width(int k, int64_t inner, int split_bits) {
 void rgemm_ozaki_dev(int k, int64_t m, int64_t n, int64_t l, View A, View B, View C, int d,
                      int width, cudaStream_t st) {
   const OpsTable* T = table_for(k);
-  // zero C (acc_plane accumulates into a fresh RealMatrix.zeros)
-  for (int c = 0; c < k; c++)
-    if (m > 0 && l > 0) ck(cudaMemset2DAsync(C.re + c * C.ps, C.ld * 8, 0, l * 8, m, st), "memset");
   if (m <= 0 || l <= 0) return;
   DevBuf ra(sizeof(double) * k * m * n, st), rb(sizeof(double) * k * n * l, st);
   DevBuf pa(sizeof(double) * d * m * n, st), pb(sizeof(double) * d * n * l, st);
   DevBuf mua(sizeof(double) * (m + 1), st), mub(sizeof(double) * (l + 1), st);
-  DevBuf sca(sizeof(double) * (m + 1), st), scb(sizeof(double) * (l + 1), st);
+  DevBuf sca(sizeof(double) * d * (m + 1), st), scb(sizeof(double) * d * (l + 1), st);
   View RA{ra.d(), nullptr, n, m * n}, RB{rb.d(), nullptr, l, n * l};
   copy_view(k, RA, A, m, n, st);
   copy_view(k, RB, B, n, l, st);
   for (int s = 0; s < d; s++) {
-    split_dispatch(k, RA, m, n, 0, mua.d(), width, pa.d() + (int64_t)s * m * n, sca.d(), st);
-    split_dispatch(k, RB, n, l, 1, mub.d(), width, pb.d() + (int64_t)s * n * l, scb.d(), st);
+    split_dispatch(k, RA, m, n, 0, mua.d(), width, pa.d() + (int64_t)s * m * n,
+                   sca.d() + (int64_t)s * m, st);
+    split_dispatch(k, RB, n, l, 1, mub.d(), width, pb.d() + (int64_t)s * n * l,
+                   scb.d() + (int64_t)s * l, st);
   }
+  const auto pairs = pair_schedule(d, width, k);
+  // exact part products on the INT8 tensor cores, acc_plane + renorm fused
+  if (ozaki_tc_enabled() &&
+      ozaki_tc_gemm(k, m, n, l, pa.d(), pb.d(), sca.d(), scb.d(), d, pairs, width, C, st))
+    return;
+  // binary64 seam: zero C (acc_plane accumulates into a fresh RealMatrix.zeros)
+  for (int c = 0; c < k; c++)
+    ck(cudaMemset2DAsync(C.re + c * C.ps, C.ld * 8, 0, l * 8, m, st), "memset");
   DevBuf P(sizeof(double) * m * l, st);
-  for (auto pq : pair_schedule(d, width, k)) {
+  for (auto pq : pairs) {
     f64_gemm(m, n, l, pa.d() + (int64_t)pq.first * m * n, n, pb.d() + (int64_t)pq.second * n * l,
              l, P.d(), l, st);
     acc_dispatch(k, C, m, l, P.d(), l, st);

@@ -1,0 +1,459 @@
+// ozaki_tc.cu -- the Ozaki scheme's exact part products on the B200 INT8
+// tensor cores (BASELINE.json north_star item 3).
+//
+// Reference: ozaki.py:79-159 (split grids, _pair_schedule, rgemm_ozaki),
+// _kernels.py:485-517 (acc_plane, renorm_planes).
+//
+// Why this is bit-identical to the reference's binary64 seam (np.matmul):
+// every entry of split part p is an integer multiple of its row (left) or
+// column (right) grid, part = I * 2^e with |I| <= 2^width (ozaki.py:54-60,
+// 97-107), and width <= (53 - ceil(log2 n)) / 2 (ozaki.py:33-38) makes
+// every part product  P = A_p B_q = 2^(ea_i + eb_j) * sum_t Ia_it Ib_tj  an
+// exact binary64 number -- the reference's GEMM returns exactly
+// J_ij * 2^(ea_i + eb_j) with the exact integer J.  Here J is formed from
+// INT8 digit slices:  I = a0 2^(2b) + a1 2^b + a2  (b = 7: all digits s8,
+// |a0| <= 64; b = 8: a0 s8, a1/a2 u8), so
+//     J = sum_{s=0..4} 2^(b(4-s)) G_s,   G_s = sum_{i+j=s} A_i B_j^T,
+// five int32 tcgen05 accumulators per pair (|G_s| < 2^31 is checked on the
+// host from n and the digit bounds), recombined in int64 (exact, |J| <=
+// 2^53), converted exactly to binary64 and scaled by the two powers of two.
+// The acc_plane insertion (schedule order) and the final renorm_planes run
+// in the same kernel on the per-thread accumulators -- one launch replaces
+// the reference's npairs GEMMs + npairs acc_plane passes + renorm pass.
+// (Subnormal grids, i.e. operands below ~1e-290, are outside this argument;
+// the split kernels already follow the reference there.)
+//
+// Kernel shape (per CTA: one 128 x BN output tile, 128 threads):
+//   * operands: K-major INT8 slices in global memory, padded to the tile
+//     grid; staged by cp.async (16 B) into a 3-stage ring in the canonical
+//     no-swizzle K-major UMMA layout (8-row x 16-byte core matrices);
+//   * one elected thread issues tcgen05.mma.cta_group::1.kind::i8
+//     (M=128, N=BN, K=32) -- 9 per 32-deep k-step into 5 TMEM accumulator
+//     groups -- and tcgen05.commit's to per-stage mbarriers, so the ring
+//     slots are recycled as soon as the tensor core has read them;
+//   * after a pair's last k-step, all 4 warps drain the groups with
+//     tcgen05.ld.32x32b (thread = output row), recombine, scale and run
+//     acc_plane into register-resident expansions; the next pair's loads
+//     are already in flight.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <utility>
+#include <vector>
+
+#include "kernels.cuh"
+#include "ozaki_tc.h"
+#include "prof.h"
+
+namespace mpc {
+namespace otc {
+
+constexpr int BM = 128;     // MMA M (one TMEM lane per output row)
+constexpr int BKB = 64;     // K bytes per pipeline stage = 2 MMAs of K = 32
+constexpr int NSL = 3;      // digit slices per part
+constexpr int NGRP = 5;     // accumulator groups s = i + j
+constexpr int NTHR = 128;   // 4 warps: loaders, epilogue; thread 0 issues MMAs
+constexpr int STAGES = 3;
+constexpr int MAXPAIRS = 160;
+
+template <int KL>
+struct Tile {
+  static constexpr int BN = KL == 2 ? 32 : 16;  // register budget of the expansions
+  static constexpr int A_BYTES = NSL * BM * BKB;
+  static constexpr int B_BYTES = NSL * BN * BKB;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE;
+  static constexpr uint32_t TCOLS = NGRP * BN <= 128 ? 128 : 256;  // power of two >= 32
+};
+
+struct Params {
+  const int8_t* sa;       // [d][NSL][Mp][Kp]
+  const int8_t* sb;       // [d][NSL][Lp][Kp]
+  const double* scale_a;  // [d][m]
+  const double* scale_b;  // [d][l]
+  int64_t m, l, Mp, Lp, Kp;
+  int npairs, shift, lo_unsigned;
+  View C;
+  unsigned char pp[MAXPAIRS], pq[MAXPAIRS];
+};
+
+MPC_DI uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+MPC_DI void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g) : "memory");
+}
+
+MPC_DI void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+MPC_DI void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+MPC_DI void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+MPC_DI void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// canonical K-major, no-swizzle shared-memory matrix descriptor: 8-row x
+// 16-byte core matrices, LBO = byte distance of the two 16-byte K halves of
+// one MMA, SBO = byte distance of consecutive 8-row groups
+MPC_DI uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, layout SWIZZLE_NONE
+}
+
+// instruction descriptor: D = s32, A/B s8 or u8, both K-major, M = 128
+__host__ __device__ constexpr uint32_t make_idesc(int n, bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+MPC_DI void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                   uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+MPC_DI void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+MPC_DI void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+MPC_DI void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// acc_plane insertion of one exact binary64 product (_kernels.py:502-517)
+template <int KL>
+MPC_DI void acc_insert(Exp<KL>& c, double q) {
+  double h[KL + 1];
+#pragma unroll
+  for (int i = KL - 1; i >= 0; i--) {
+    double s, e;
+    two_sum(q, c.c[i], s, e);
+    q = s;
+    h[i + 1] = e;
+  }
+  h[0] = q;
+#pragma unroll
+  for (int i = 0; i < KL; i++) c.c[i] = h[i];
+}
+
+template <int KL>
+__global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant__ Params P) {
+  using T = Tile<KL>;
+  constexpr int BN = T::BN;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar[STAGES];
+  __shared__ __align__(8) uint64_t mbar_acc;
+  __shared__ uint32_t tmem_slot;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t col0 = (int64_t)blockIdx.x * BN;
+  const int64_t row0 = (int64_t)blockIdx.y * BM;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; s++) mbar_init(&mbar[s], 1);
+    mbar_init(&mbar_acc, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(T::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  const uint32_t sbase = smem_u32(smem);
+  const int nk = (int)(P.Kp / BKB);
+  const int total = P.npairs * nk;
+  const int64_t slA = P.Mp * P.Kp, slB = P.Lp * P.Kp;
+
+  auto load_chunk = [&](int c) {
+    const int t = c / nk, kc = c % nk;
+    const uint32_t sA = sbase + (uint32_t)((c % STAGES) * T::STAGE), sB = sA + T::A_BYTES;
+    const int8_t* ga = P.sa + (int64_t)P.pp[t] * NSL * slA + row0 * P.Kp + (int64_t)kc * BKB;
+#pragma unroll
+    for (int it = 0; it < NSL * BM * 4 / NTHR; it++) {
+      const int e = tid + it * NTHR;
+      const int i = e / (BM * 4), r = (e >> 2) % BM, q = e & 3;
+      cp_async16(sA + i * (BM * BKB) + q * (BM * 16) + r * 16,
+                 ga + i * slA + (int64_t)r * P.Kp + q * 16);
+    }
+    const int8_t* gb = P.sb + (int64_t)P.pq[t] * NSL * slB + col0 * P.Kp + (int64_t)kc * BKB;
+#pragma unroll
+    for (int it = 0; it < (NSL * BN * 4 + NTHR - 1) / NTHR; it++) {
+      const int e = tid + it * NTHR;
+      if (e < NSL * BN * 4) {
+        const int j = e / (BN * 4), r = (e >> 2) % BN, q = e & 3;
+        cp_async16(sB + j * (BN * BKB) + q * (BN * 16) + r * 16,
+                   gb + j * slB + (int64_t)r * P.Kp + q * 16);
+      }
+    }
+  };
+
+  Exp<KL> acc[BN];
+#pragma unroll
+  for (int j = 0; j < BN; j++) acc[j] = exp_zero<KL>();
+  const int64_t grow = row0 + warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+
+#pragma unroll 1
+  for (int c = 0; c < STAGES - 1; c++) {
+    if (c < total) load_chunk(c);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+
+#pragma unroll 1
+  for (int c = 0; c < total; c++) {
+    const int cn = c + STAGES - 1;
+    if (cn < total) {
+      // the slot of chunk cn was last read by the MMAs of chunk c - 1
+      if (c >= 1) mbar_wait(&mbar[(c - 1) % STAGES], (uint32_t)(((c - 1) / STAGES) & 1));
+      load_chunk(cn);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 1) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    const int t = c / nk, kc = c % nk;
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sA = sbase + (uint32_t)((c % STAGES) * T::STAGE), sB = sA + T::A_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < BKB / 32; ks++) {
+#pragma unroll
+        for (int i = 0; i < NSL; i++) {
+#pragma unroll
+          for (int j = 0; j < NSL; j++) {
+            const uint64_t ad = make_desc(sA + i * (BM * BKB) + ks * 2 * (BM * 16), BM * 16, 128);
+            const uint64_t bd = make_desc(sB + j * (BN * BKB) + ks * 2 * (BN * 16), BN * 16, 128);
+            // first write into group i + j of this pair: (0,0) (0,1) (0,2) (1,2) (2,2)
+            const uint32_t accum = (kc == 0 && ks == 0 && (i == 0 || j == NSL - 1)) ? 0u : 1u;
+            const uint32_t id = make_idesc(BN, i == 0 || !P.lo_unsigned, j == 0 || !P.lo_unsigned);
+            mma_i8(tmem + (uint32_t)((i + j) * BN), ad, bd, id, accum);
+          }
+        }
+      }
+      mma_commit(&mbar[c % STAGES]);
+      if (kc == nk - 1) mma_commit(&mbar_acc);
+    }
+    __syncwarp();
+    if (kc == nk - 1) {
+      // epilogue of pair t: J = sum_s 2^(b(4-s)) G_s, P = J 2^ea 2^eb, acc_plane
+      mbar_wait(&mbar_acc, (uint32_t)(t & 1));
+      tc_fence_after();
+      const double sav = grow < P.m ? P.scale_a[(int64_t)P.pp[t] * P.m + grow] : 0.0;
+      const double* sbp = P.scale_b + (int64_t)P.pq[t] * P.l;
+      const int b = P.shift;
+#pragma unroll
+      for (int cc = 0; cc < BN / 8; cc++) {
+        uint32_t r[NGRP][8];
+#pragma unroll
+        for (int g = 0; g < NGRP; g++) tmem_ld8(trow + (uint32_t)(g * BN + cc * 8), r[g]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 8; jj++) {
+          long long J = (long long)(int)r[0][jj];
+#pragma unroll
+          for (int g = 1; g < NGRP; g++) J = J * (1ll << b) + (long long)(int)r[g][jj];
+          const int64_t gc = col0 + cc * 8 + jj;
+          const double sbv = gc < P.l ? sbp[gc] : 0.0;
+          const double v = __dmul_rn(__dmul_rn(__ll2double_rn(J), sav), sbv);
+          acc_insert<KL>(acc[cc * 8 + jj], v);
+        }
+      }
+      tc_fence_before();
+      __syncthreads();  // every TMEM read done before the next pair overwrites
+    }
+  }
+
+  // renorm_planes (_kernels.py:485-499) and store
+  if (grow < P.m) {
+#pragma unroll
+    for (int j = 0; j < BN; j++) {
+      const int64_t gc = col0 + j;
+      if (gc < P.l) {
+        double buf[KL];
+#pragma unroll
+        for (int c = 0; c < KL; c++) buf[c] = acc[j].c[c];
+        Exp<KL> o = renorm<KL, KL>(buf, KL);
+        stexp_<KL>(P.C.re + grow * P.C.ld + gc, P.C.ps, o);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(T::TCOLS));
+}
+
+// part (row-major, ld) -> NSL digit slices, K-major and padded:
+// side 0 (left):  out[s][i][t] from part[i][t] / scale[i]   (R = rows, Kd = cols)
+// side 1 (right): out[s][j][t] from part[t][j] / scale[j]   (R = cols, Kd = rows)
+// one thread per (r, 16-deep group of t); the buffer was zeroed beforehand
+__global__ void slice_kernel(const double* part, int64_t rows, int64_t cols, int64_t ld,
+                             const double* scale, int side, int shift, int8_t* out, int64_t Rp,
+                             int64_t Kp) {
+  const int64_t R = side == 0 ? rows : cols, Kd = side == 0 ? cols : rows;
+  const int64_t ng = (Kd + 15) / 16;
+  const int64_t mask = (1ll << shift) - 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < R * ng;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = side == 0 ? e / ng : e % R;
+    const int64_t g = side == 0 ? e % ng : e / R;
+    int es = 0;
+    frexp(scale[r], &es);
+    es -= 1;  // scale = 2^es (a power of two by construction, ozaki.py:107)
+    union {
+      int8_t b[16];
+      int4 v;
+    } d0, d1, d2;
+#pragma unroll
+    for (int tt = 0; tt < 16; tt++) {
+      const int64_t t = g * 16 + tt;
+      long long I = 0;
+      if (t < Kd) {
+        const double x = side == 0 ? part[r * ld + t] : part[t * ld + r];
+        I = __double2ll_rn(ldexp(x, -es));  // exact: x is an integer multiple of 2^es
+      }
+      d0.b[tt] = (int8_t)(I >> (2 * shift));
+      d1.b[tt] = (int8_t)(uint8_t)((I >> shift) & mask);
+      d2.b[tt] = (int8_t)(uint8_t)(I & mask);
+    }
+    int8_t* o = out + r * Kp + g * 16;
+    *reinterpret_cast<int4*>(o) = d0.v;
+    *reinterpret_cast<int4*>(o + Rp * Kp) = d1.v;
+    *reinterpret_cast<int4*>(o + 2 * Rp * Kp) = d2.v;
+  }
+}
+
+unsigned grid_for(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+template <int KL>
+void launch(const Params& P, cudaStream_t st, double ops) {
+  using T = Tile<KL>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ozaki_tc_kernel<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    attr = true;
+  }
+  dim3 grid((unsigned)(P.Lp / T::BN), (unsigned)(P.Mp / BM));
+  int tok = prof_begin(PC_GEMM, ops, st);
+  ozaki_tc_kernel<KL><<<grid, NTHR, T::SMEM, st>>>(P);
+  prof_end(tok, st);
+  check_launch("ozaki_tc_kernel");
+}
+
+}  // namespace otc
+
+bool ozaki_tc_enabled() {
+  const char* e = getenv("MPC_OZAKI_GEMM");
+  return !(e && strcmp(e, "dgemm") == 0);
+}
+
+bool ozaki_tc_gemm(int k, int64_t m, int64_t n, int64_t l, const double* parts_a,
+                   const double* parts_b, const double* scale_a, const double* scale_b, int d,
+                   const std::vector<std::pair<int, int>>& pairs, int width, View C,
+                   cudaStream_t st) {
+  using namespace otc;
+  if (k < 2 || k > 4 || m <= 0 || l <= 0 || n <= 0) return false;
+  if ((int)pairs.size() > MAXPAIRS || d > 255) return false;
+  // digit base and the int32 headroom of the largest accumulator group
+  int shift;
+  double gmax;
+  if (width <= 20) {
+    shift = 7;       // |a0| <= 2^20 / 2^14 = 64, a1, a2 in [0, 127]: all s8
+    gmax = 32385.0;  // 64*127 + 127*127 + 127*64
+  } else if (width <= 22) {
+    shift = 8;        // |a0| <= 64 (s8), a1, a2 in [0, 255] (u8)
+    gmax = 130050.0;  // 255*255*2
+  } else {
+    return false;
+  }
+  if (gmax * (double)n >= 2147483648.0) return false;
+  const int BN = k == 2 ? Tile<2>::BN : Tile<3>::BN;
+  const int64_t Mp = (m + BM - 1) / BM * BM, Lp = (l + BN - 1) / BN * BN,
+                Kp = (n + BKB - 1) / BKB * BKB;
+  const size_t bytes_a = (size_t)d * NSL * Mp * Kp, bytes_b = (size_t)d * NSL * Lp * Kp;
+  int8_t* buf = nullptr;
+  if (cudaMallocAsync((void**)&buf, bytes_a + bytes_b, st) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaMemsetAsync(buf, 0, bytes_a + bytes_b, st);
+  int8_t* sa = buf;
+  int8_t* sb = buf + bytes_a;
+  int tok = prof_begin(PC_OTHER, 0.0, st);
+  for (int p = 0; p < d; p++) {
+    slice_kernel<<<grid_for(m * ((n + 15) / 16)), 256, 0, st>>>(
+        parts_a + (int64_t)p * m * n, m, n, n, scale_a + (int64_t)p * m, 0, shift,
+        sa + (int64_t)p * NSL * Mp * Kp, Mp, Kp);
+    slice_kernel<<<grid_for(l * ((n + 15) / 16)), 256, 0, st>>>(
+        parts_b + (int64_t)p * n * l, n, l, l, scale_b + (int64_t)p * l, 1, shift,
+        sb + (int64_t)p * NSL * Lp * Kp, Lp, Kp);
+  }
+  prof_end(tok, st);
+  check_launch("ozaki slice_kernel");
+  Params P;
+  memset(&P, 0, sizeof(P));
+  P.sa = sa;
+  P.sb = sb;
+  P.scale_a = scale_a;
+  P.scale_b = scale_b;
+  P.m = m;
+  P.l = l;
+  P.Mp = Mp;
+  P.Lp = Lp;
+  P.Kp = Kp;
+  P.npairs = (int)pairs.size();
+  P.shift = shift;
+  P.lo_unsigned = shift == 8 ? 1 : 0;
+  P.C = C;
+  for (size_t i = 0; i < pairs.size(); i++) {
+    P.pp[i] = (unsigned char)pairs[i].first;
+    P.pq[i] = (unsigned char)pairs[i].second;
+  }
+  // INT8 tensor-core ops issued (2 per MAC, NSL^2 slice products per pair)
+  const double ops = 2.0 * NSL * NSL * (double)pairs.size() * (double)m * (double)n * (double)l;
+  switch (k) {
+    case 2: launch<2>(P, st, ops); break;
+    case 3: launch<3>(P, st, ops); break;
+    default: launch<4>(P, st, ops); break;
+  }
+  cudaFreeAsync(buf, st);
+  return true;
+}
+
+}  // namespace mpc
