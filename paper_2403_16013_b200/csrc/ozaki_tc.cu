@@ -53,23 +53,24 @@ constexpr int BM = 128;     // MMA M (one TMEM lane per output row)
 constexpr int BKB = 64;     // K bytes per pipeline stage = 2 MMAs of K = 32
 constexpr int NSL = 3;      // digit slices per part
 constexpr int NGRP = 5;     // accumulator groups s = i + j
-constexpr int NTHR = 128;   // 4 warps: loaders, epilogue; thread 0 issues MMAs
-constexpr int STAGES = 3;
+constexpr int NEPI = 8;     // epilogue warps (2 per TMEM lane quadrant)
+constexpr int NTHR = (NEPI + 2) * 32;  // + producer warp + MMA warp
 constexpr int MAXPAIRS = 160;
+constexpr uint32_t TCOLS = 512;        // two accumulator buffers at columns 0 / 256
 
 template <int KL>
 struct Tile {
-  static constexpr int BN = KL == 2 ? 32 : 16;  // register budget of the expansions
+  static constexpr int BN = KL == 2 ? 48 : 32;  // 5 * BN <= 256: double-buffered TMEM
   static constexpr int A_BYTES = NSL * BM * BKB;
   static constexpr int B_BYTES = NSL * BN * BKB;
   static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (220 * 1024) / STAGE;
   static constexpr int SMEM = STAGES * STAGE;
-  static constexpr uint32_t TCOLS = NGRP * BN <= 128 ? 128 : 256;  // power of two >= 32
 };
 
 struct Params {
-  const int8_t* sa;       // [d][NSL][Mp][Kp]
-  const int8_t* sb;       // [d][NSL][Lp][Kp]
+  const int8_t* sa;       // [d][NSL][Mp/BM][Kp/16][BM][16]  (stage-contiguous tiles)
+  const int8_t* sb;       // [d][NSL][Lp/BN][Kp/16][BN][16]
   const double* scale_a;  // [d][m]
   const double* scale_b;  // [d][l]
   int64_t m, l, Mp, Lp, Kp;
@@ -79,10 +80,6 @@ struct Params {
 };
 
 MPC_DI uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-MPC_DI void cp_async16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g) : "memory");
-}
 
 MPC_DI void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -97,6 +94,25 @@ MPC_DI void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
+      : "memory");
+}
+
+MPC_DI void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+MPC_DI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// bulk global -> shared copy, completion counted on the mbarrier (async proxy)
+MPC_DI void bulk_g2s(uint32_t sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          sdst),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -162,170 +178,192 @@ MPC_DI void acc_insert(Exp<KL>& c, double q) {
   for (int i = 0; i < KL; i++) c.c[i] = h[i];
 }
 
+// Warp roles: warps 0..7 epilogue (warp w drains TMEM lane quadrant w % 4,
+// column half w / 4), warp 8 producer (one lane issues the bulk copies),
+// warp 9 MMA issuer (one lane).  Pipelines: smem ring full/empty (bulk copy
+// -> MMA -> tcgen05.commit), TMEM double buffer full/empty (MMA -> epilogue).
 template <int KL>
 __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant__ Params P) {
   using T = Tile<KL>;
-  constexpr int BN = T::BN;
+  constexpr int BN = T::BN, S = T::STAGES, HALF = BN / 2;
+  static_assert(HALF % 8 == 0, "column half must be a multiple of the x8 TMEM load");
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[STAGES];
-  __shared__ __align__(8) uint64_t mbar_acc;
+  __shared__ __align__(8) uint64_t full[S], empty[S], accf[2], acce[2];
   __shared__ uint32_t tmem_slot;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t col0 = (int64_t)blockIdx.x * BN;
-  const int64_t row0 = (int64_t)blockIdx.y * BM;
+  const int64_t ct = blockIdx.x, rt = blockIdx.y;  // column tile, row tile
+  const int64_t col0 = ct * BN, row0 = rt * BM;
 
   if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; s++) mbar_init(&mbar[s], 1);
-    mbar_init(&mbar_acc, 1);
+    for (int s = 0; s < S; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], NEPI * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_u32(&tmem_slot)),
-                 "r"(T::TCOLS));
+                 "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-
   const uint32_t sbase = smem_u32(smem);
   const int nk = (int)(P.Kp / BKB);
-  const int total = P.npairs * nk;
-  const int64_t slA = P.Mp * P.Kp, slB = P.Lp * P.Kp;
+  const int64_t kch = P.Kp / 16;
 
-  auto load_chunk = [&](int c) {
-    const int t = c / nk, kc = c % nk;
-    const uint32_t sA = sbase + (uint32_t)((c % STAGES) * T::STAGE), sB = sA + T::A_BYTES;
-    const int8_t* ga = P.sa + (int64_t)P.pp[t] * NSL * slA + row0 * P.Kp + (int64_t)kc * BKB;
+  if (warp == NEPI) {
+    // ---------------- producer: one lane streams the stage-contiguous slices
+    if (lane == 0) {
+      const int64_t tilesA = P.Mp / BM, tilesB = P.Lp / BN;
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < P.npairs; t++) {
+        const int8_t* ga = P.sa + (((int64_t)P.pp[t] * NSL * tilesA + rt) * kch) * (BM * 16);
+        const int8_t* gb = P.sb + (((int64_t)P.pq[t] * NSL * tilesB + ct) * kch) * (BN * 16);
+        for (int kc = 0; kc < nk; kc++) {
+          mbar_wait(&empty[slot], ph ^ 1u);
+          const uint32_t sA = sbase + (uint32_t)(slot * T::STAGE), sB = sA + T::A_BYTES;
+          mbar_expect_tx(&full[slot], (uint32_t)T::STAGE);
 #pragma unroll
-    for (int it = 0; it < NSL * BM * 4 / NTHR; it++) {
-      const int e = tid + it * NTHR;
-      const int i = e / (BM * 4), r = (e >> 2) % BM, q = e & 3;
-      cp_async16(sA + i * (BM * BKB) + q * (BM * 16) + r * 16,
-                 ga + i * slA + (int64_t)r * P.Kp + q * 16);
-    }
-    const int8_t* gb = P.sb + (int64_t)P.pq[t] * NSL * slB + col0 * P.Kp + (int64_t)kc * BKB;
+          for (int i = 0; i < NSL; i++)
+            bulk_g2s(sA + i * (BM * BKB), ga + ((int64_t)i * tilesA * kch + kc * 4) * (BM * 16),
+                     BM * BKB, &full[slot]);
 #pragma unroll
-    for (int it = 0; it < (NSL * BN * 4 + NTHR - 1) / NTHR; it++) {
-      const int e = tid + it * NTHR;
-      if (e < NSL * BN * 4) {
-        const int j = e / (BN * 4), r = (e >> 2) % BN, q = e & 3;
-        cp_async16(sB + j * (BN * BKB) + q * (BN * 16) + r * 16,
-                   gb + j * slB + (int64_t)r * P.Kp + q * 16);
-      }
-    }
-  };
-
-  Exp<KL> acc[BN];
-#pragma unroll
-  for (int j = 0; j < BN; j++) acc[j] = exp_zero<KL>();
-  const int64_t grow = row0 + warp * 32 + lane;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-
-#pragma unroll 1
-  for (int c = 0; c < STAGES - 1; c++) {
-    if (c < total) load_chunk(c);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
-
-#pragma unroll 1
-  for (int c = 0; c < total; c++) {
-    const int cn = c + STAGES - 1;
-    if (cn < total) {
-      // the slot of chunk cn was last read by the MMAs of chunk c - 1
-      if (c >= 1) mbar_wait(&mbar[(c - 1) % STAGES], (uint32_t)(((c - 1) / STAGES) & 1));
-      load_chunk(cn);
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 1) : "memory");
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    __syncthreads();
-    const int t = c / nk, kc = c % nk;
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t sA = sbase + (uint32_t)((c % STAGES) * T::STAGE), sB = sA + T::A_BYTES;
-#pragma unroll
-      for (int ks = 0; ks < BKB / 32; ks++) {
-#pragma unroll
-        for (int i = 0; i < NSL; i++) {
-#pragma unroll
-          for (int j = 0; j < NSL; j++) {
-            const uint64_t ad = make_desc(sA + i * (BM * BKB) + ks * 2 * (BM * 16), BM * 16, 128);
-            const uint64_t bd = make_desc(sB + j * (BN * BKB) + ks * 2 * (BN * 16), BN * 16, 128);
-            // first write into group i + j of this pair: (0,0) (0,1) (0,2) (1,2) (2,2)
-            const uint32_t accum = (kc == 0 && ks == 0 && (i == 0 || j == NSL - 1)) ? 0u : 1u;
-            const uint32_t id = make_idesc(BN, i == 0 || !P.lo_unsigned, j == 0 || !P.lo_unsigned);
-            mma_i8(tmem + (uint32_t)((i + j) * BN), ad, bd, id, accum);
+          for (int j = 0; j < NSL; j++)
+            bulk_g2s(sB + j * (BN * BKB), gb + ((int64_t)j * tilesB * kch + kc * 4) * (BN * 16),
+                     BN * BKB, &full[slot]);
+          if (++slot == S) {
+            slot = 0;
+            ph ^= 1u;
           }
         }
       }
-      mma_commit(&mbar[c % STAGES]);
-      if (kc == nk - 1) mma_commit(&mbar_acc);
     }
-    __syncwarp();
-    if (kc == nk - 1) {
-      // epilogue of pair t: J = sum_s 2^(b(4-s)) G_s, P = J 2^ea 2^eb, acc_plane
-      mbar_wait(&mbar_acc, (uint32_t)(t & 1));
+  } else if (warp == NEPI + 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < P.npairs; t++) {
+        const int buf = t & 1;
+        mbar_wait(&acce[buf], (uint32_t)(((t >> 1) & 1) ^ 1));  // epilogue drained it
+        tc_fence_after();
+        const uint32_t tacc = tmem + (uint32_t)(buf * 256);
+        for (int kc = 0; kc < nk; kc++) {
+          mbar_wait(&full[slot], ph);
+          tc_fence_after();
+          const uint32_t sA = sbase + (uint32_t)(slot * T::STAGE), sB = sA + T::A_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BKB / 32; ks++) {
+#pragma unroll
+            for (int i = 0; i < NSL; i++) {
+#pragma unroll
+              for (int j = 0; j < NSL; j++) {
+                const uint64_t ad =
+                    make_desc(sA + i * (BM * BKB) + ks * 2 * (BM * 16), BM * 16, 128);
+                const uint64_t bd =
+                    make_desc(sB + j * (BN * BKB) + ks * 2 * (BN * 16), BN * 16, 128);
+                // first write into group i + j of this pair: (0,0) (0,1) (0,2) (1,2) (2,2)
+                const uint32_t accum = (kc == 0 && ks == 0 && (i == 0 || j == NSL - 1)) ? 0u : 1u;
+                const uint32_t id =
+                    make_idesc(BN, i == 0 || !P.lo_unsigned, j == 0 || !P.lo_unsigned);
+                mma_i8(tacc + (uint32_t)((i + j) * BN), ad, bd, id, accum);
+              }
+            }
+          }
+          mma_commit(&empty[slot]);  // slot free once these MMAs have read it
+          if (++slot == S) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+        mma_commit(&accf[buf]);  // accumulators of pair t complete
+      }
+    }
+  } else {
+    // ---------------- epilogue: J = sum_s 2^(b(4-s)) G_s, P = J 2^ea 2^eb, acc_plane
+    const int quad = warp & 3, half = warp >> 2;
+    const int64_t grow = row0 + quad * 32 + lane;
+    const int cbase = half * HALF;
+    Exp<KL> acc[HALF];
+#pragma unroll
+    for (int j = 0; j < HALF; j++) acc[j] = exp_zero<KL>();
+    const int b = P.shift;
+    for (int t = 0; t < P.npairs; t++) {
+      const int buf = t & 1;
+      mbar_wait(&accf[buf], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
+      const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * 256 + cbase);
       const double sav = grow < P.m ? P.scale_a[(int64_t)P.pp[t] * P.m + grow] : 0.0;
       const double* sbp = P.scale_b + (int64_t)P.pq[t] * P.l;
-      const int b = P.shift;
 #pragma unroll
-      for (int cc = 0; cc < BN / 8; cc++) {
+      for (int cc = 0; cc < HALF / 8; cc++) {
         uint32_t r[NGRP][8];
 #pragma unroll
         for (int g = 0; g < NGRP; g++) tmem_ld8(trow + (uint32_t)(g * BN + cc * 8), r[g]);
         tmem_wait_ld();
+        if (cc == HALF / 8 - 1) {
+          tc_fence_before();
+          mbar_arrive(&acce[buf]);  // this thread's TMEM reads of pair t are done
+        }
 #pragma unroll
         for (int jj = 0; jj < 8; jj++) {
           long long J = (long long)(int)r[0][jj];
 #pragma unroll
           for (int g = 1; g < NGRP; g++) J = J * (1ll << b) + (long long)(int)r[g][jj];
-          const int64_t gc = col0 + cc * 8 + jj;
+          const int64_t gc = col0 + cbase + cc * 8 + jj;
           const double sbv = gc < P.l ? sbp[gc] : 0.0;
           const double v = __dmul_rn(__dmul_rn(__ll2double_rn(J), sav), sbv);
           acc_insert<KL>(acc[cc * 8 + jj], v);
         }
       }
-      tc_fence_before();
-      __syncthreads();  // every TMEM read done before the next pair overwrites
     }
-  }
-
-  // renorm_planes (_kernels.py:485-499) and store
-  if (grow < P.m) {
+    // renorm_planes (_kernels.py:485-499) and store
+    if (grow < P.m) {
 #pragma unroll
-    for (int j = 0; j < BN; j++) {
-      const int64_t gc = col0 + j;
-      if (gc < P.l) {
-        double buf[KL];
+      for (int j = 0; j < HALF; j++) {
+        const int64_t gc = col0 + cbase + j;
+        if (gc < P.l) {
+          double bufv[KL];
 #pragma unroll
-        for (int c = 0; c < KL; c++) buf[c] = acc[j].c[c];
-        Exp<KL> o = renorm<KL, KL>(buf, KL);
-        stexp_<KL>(P.C.re + grow * P.C.ld + gc, P.C.ps, o);
+          for (int c = 0; c < KL; c++) bufv[c] = acc[j].c[c];
+          Exp<KL> o = renorm<KL, KL>(bufv, KL);
+          stexp_<KL>(P.C.re + grow * P.C.ld + gc, P.C.ps, o);
+        }
       }
     }
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0)
+  if (warp == 0) {
+    tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(T::TCOLS));
+                 "r"(TCOLS));
+  }
 }
 
-// part (row-major, ld) -> NSL digit slices, K-major and padded:
-// side 0 (left):  out[s][i][t] from part[i][t] / scale[i]   (R = rows, Kd = cols)
-// side 1 (right): out[s][j][t] from part[t][j] / scale[j]   (R = cols, Kd = rows)
+// part (row-major, ld) -> NSL digit slices in the stage-contiguous tiled
+// layout [s][R/TR][Kp/16][TR][16] (TR = BM for the left operand, BN for the
+// right one):
+// side 0 (left):  element (i, t) from part[i][t] / scale[i]   (R = rows, Kd = cols)
+// side 1 (right): element (j, t) from part[t][j] / scale[j]   (R = cols, Kd = rows)
 // one thread per (r, 16-deep group of t); the buffer was zeroed beforehand
 __global__ void slice_kernel(const double* part, int64_t rows, int64_t cols, int64_t ld,
                              const double* scale, int side, int shift, int8_t* out, int64_t Rp,
-                             int64_t Kp) {
+                             int64_t Kp, int TR) {
   const int64_t R = side == 0 ? rows : cols, Kd = side == 0 ? cols : rows;
   const int64_t ng = (Kd + 15) / 16;
   const int64_t mask = (1ll << shift) - 1;
+  const int64_t kch = Kp / 16, slice = Rp * Kp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < R * ng;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = side == 0 ? e / ng : e % R;
@@ -349,10 +387,10 @@ __global__ void slice_kernel(const double* part, int64_t rows, int64_t cols, int
       d1.b[tt] = (int8_t)(uint8_t)((I >> shift) & mask);
       d2.b[tt] = (int8_t)(uint8_t)(I & mask);
     }
-    int8_t* o = out + r * Kp + g * 16;
+    int8_t* o = out + ((r / TR) * kch + g) * (TR * 16) + (r % TR) * 16;
     *reinterpret_cast<int4*>(o) = d0.v;
-    *reinterpret_cast<int4*>(o + Rp * Kp) = d1.v;
-    *reinterpret_cast<int4*>(o + 2 * Rp * Kp) = d2.v;
+    *reinterpret_cast<int4*>(o + slice) = d1.v;
+    *reinterpret_cast<int4*>(o + 2 * slice) = d2.v;
   }
 }
 
@@ -419,10 +457,10 @@ bool ozaki_tc_gemm(int k, int64_t m, int64_t n, int64_t l, const double* parts_a
   for (int p = 0; p < d; p++) {
     slice_kernel<<<grid_for(m * ((n + 15) / 16)), 256, 0, st>>>(
         parts_a + (int64_t)p * m * n, m, n, n, scale_a + (int64_t)p * m, 0, shift,
-        sa + (int64_t)p * NSL * Mp * Kp, Mp, Kp);
+        sa + (int64_t)p * NSL * Mp * Kp, Mp, Kp, BM);
     slice_kernel<<<grid_for(l * ((n + 15) / 16)), 256, 0, st>>>(
         parts_b + (int64_t)p * n * l, n, l, l, scale_b + (int64_t)p * l, 1, shift,
-        sb + (int64_t)p * NSL * Lp * Kp, Lp, Kp);
+        sb + (int64_t)p * NSL * Lp * Kp, Lp, Kp, BN);
   }
   prof_end(tok, st);
   check_launch("ozaki slice_kernel");
