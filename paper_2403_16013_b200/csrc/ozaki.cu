@@ -247,6 +247,9 @@ void rgemm_ozaki_dev(int k, int64_t m, int64_t n, int64_t l, View A, View B, Vie
                      int width, cudaStream_t st) {
   const OpsTable* T = table_for(k);
   if (m <= 0 || l <= 0) return;
+  const auto pairs = pair_schedule(d, width, k);
+  // fused split + exact part products on the INT8 tensor cores + acc_plane + renorm
+  if (ozaki_tc_enabled() && ozaki_tc_rgemm(k, m, n, l, A, B, C, d, pairs, width, st)) return;
   DevBuf ra(sizeof(double) * k * m * n, st), rb(sizeof(double) * k * n * l, st);
   DevBuf pa(sizeof(double) * d * m * n, st), pb(sizeof(double) * d * n * l, st);
   DevBuf mua(sizeof(double) * (m + 1), st), mub(sizeof(double) * (l + 1), st);
@@ -260,11 +263,6 @@ void rgemm_ozaki_dev(int k, int64_t m, int64_t n, int64_t l, View A, View B, Vie
     split_dispatch(k, RB, n, l, 1, mub.d(), width, pb.d() + (int64_t)s * n * l,
                    scb.d() + (int64_t)s * l, st);
   }
-  const auto pairs = pair_schedule(d, width, k);
-  // exact part products on the INT8 tensor cores, acc_plane + renorm fused
-  if (ozaki_tc_enabled() &&
-      ozaki_tc_gemm(k, m, n, l, pa.d(), pb.d(), sca.d(), scb.d(), d, pairs, width, C, st))
-    return;
   // binary64 seam: zero C (acc_plane accumulates into a fresh RealMatrix.zeros)
   for (int c = 0; c < k; c++)
     ck(cudaMemset2DAsync(C.re + c * C.ps, C.ld * 8, 0, l * 8, m, st), "memset");

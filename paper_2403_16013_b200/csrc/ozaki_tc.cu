@@ -39,6 +39,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -394,6 +395,86 @@ __global__ void slice_kernel(const double* part, int64_t rows, int64_t cols, int
   }
 }
 
+// Fused ozaki_split (ozaki.py:79-108) of one operand, straight to digit
+// slices: one CTA per grid line (a row of the left operand, a column of the
+// right one), its k-limb residual held in shared memory for all d steps:
+//   mu = max |r0| (block reduction), (f, ex) = frexp(mu), S = 2^ex 2^(53-width),
+//   part = (r0 + S) - S, r0 -= part, renorm the limbs (renorm_planes),
+//   scale = 2^(ex - width), I = part / scale -> NSL digits (tiled layout).
+// The element sequence of each step is the reference's, elementwise, so the
+// parts and grids are bit-identical to ozaki_split's.
+// src element (r, t): trans == 0 -> src[r*ld + t] (left: rows of A),
+//                     trans == 1 -> src[t*ld + r] (right: columns of B).
+template <int KL>
+__global__ void __launch_bounds__(256) split_lines_kernel(const double* src, int64_t ld, int64_t ps,
+                                                          int trans, int64_t R, int64_t n, int d,
+                                                          int width, int shift, int8_t* out,
+                                                          int64_t Rp, int64_t Kp, int TR,
+                                                          double* scale) {
+  extern __shared__ double res[];  // [KL][n]
+  __shared__ double red[8];
+  const int64_t r = blockIdx.x;
+  const int tid = threadIdx.x;
+  for (int64_t t = tid; t < n; t += blockDim.x)
+#pragma unroll
+    for (int c = 0; c < KL; c++)
+      res[c * n + t] = trans ? src[c * ps + t * ld + r] : src[c * ps + r * ld + t];
+  __syncthreads();
+  const int64_t kch = Kp / 16, slice = Rp * Kp;
+  const int64_t mask = (1ll << shift) - 1;
+  const double shiftS = ldexp(1.0, 53 - width);
+  for (int p = 0; p < d; p++) {
+    double m = 0.0;
+    for (int64_t t = tid; t < n; t += blockDim.x) m = fmax(m, fabs(res[t]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    m = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; w++) m = fmax(m, red[w]);
+    __syncthreads();  // red reused next step
+    int ex = 0;
+    frexp(m, &ex);
+    const double w = ldexp(1.0, ex);
+    const double S = __dmul_rn(w, shiftS);
+    const int es = ex - width;  // scale = ldexp(w, -width) = 2^es
+    if (tid == 0) scale[(int64_t)p * R + r] = ldexp(w, -width);
+    int8_t* o = out + (int64_t)p * NSL * slice + ((r / TR) * kch) * (TR * 16) + (r % TR) * 16;
+    for (int64_t g = tid; g < (n + 15) / 16; g += blockDim.x) {
+      union {
+        int8_t b[16];
+        int4 v;
+      } d0, d1, d2;
+#pragma unroll
+      for (int tt = 0; tt < 16; tt++) {
+        const int64_t t = g * 16 + tt;
+        long long I = 0;
+        if (t < n) {
+          const double r0 = res[t];
+          const double pt = __dsub_rn(__dadd_rn(r0, S), S);
+          double buf[KL];
+          buf[0] = __dsub_rn(r0, pt);
+#pragma unroll
+          for (int c = 1; c < KL; c++) buf[c] = res[c * n + t];
+          Exp<KL> e = renorm<KL, KL>(buf, KL);
+#pragma unroll
+          for (int c = 0; c < KL; c++) res[c * n + t] = e.c[c];
+          I = __double2ll_rn(ldexp(pt, -es));  // exact: pt is a multiple of 2^es
+        }
+        d0.b[tt] = (int8_t)(I >> (2 * shift));
+        d1.b[tt] = (int8_t)(uint8_t)((I >> shift) & mask);
+        d2.b[tt] = (int8_t)(uint8_t)(I & mask);
+      }
+      int8_t* og = o + g * (TR * 16);
+      *reinterpret_cast<int4*>(og) = d0.v;
+      *reinterpret_cast<int4*>(og + slice) = d1.v;
+      *reinterpret_cast<int4*>(og + 2 * slice) = d2.v;
+    }
+    __syncthreads();
+  }
+}
+
 unsigned grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -484,6 +565,98 @@ bool ozaki_tc_gemm(int k, int64_t m, int64_t n, int64_t l, const double* parts_a
     P.pq[i] = (unsigned char)pairs[i].second;
   }
   // INT8 tensor-core ops issued (2 per MAC, NSL^2 slice products per pair)
+  const double ops = 2.0 * NSL * NSL * (double)pairs.size() * (double)m * (double)n * (double)l;
+  switch (k) {
+    case 2: launch<2>(P, st, ops); break;
+    case 3: launch<3>(P, st, ops); break;
+    default: launch<4>(P, st, ops); break;
+  }
+  cudaFreeAsync(buf, st);
+  return true;
+}
+
+bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View C, int d,
+                    const std::vector<std::pair<int, int>>& pairs, int width, cudaStream_t st) {
+  using namespace otc;
+  if (k < 2 || k > 4 || m <= 0 || l <= 0 || n <= 0) return false;
+  if ((int)pairs.size() > MAXPAIRS || d > 255) return false;
+  int shift;
+  double gmax;
+  if (width <= 20) {
+    shift = 7;
+    gmax = 32385.0;
+  } else if (width <= 22) {
+    shift = 8;
+    gmax = 130050.0;
+  } else {
+    return false;
+  }
+  if (gmax * (double)n >= 2147483648.0) return false;
+  const size_t line_smem = sizeof(double) * (size_t)k * (size_t)n;
+  if (line_smem > 200 * 1024) return false;
+  const int BN = k == 2 ? Tile<2>::BN : Tile<3>::BN;
+  const int64_t Mp = (m + BM - 1) / BM * BM, Lp = (l + BN - 1) / BN * BN,
+                Kp = (n + BKB - 1) / BKB * BKB;
+  const size_t bytes_a = (size_t)d * NSL * Mp * Kp, bytes_b = (size_t)d * NSL * Lp * Kp;
+  const size_t bytes_s = sizeof(double) * (size_t)d * (size_t)(m + l);
+  int8_t* buf = nullptr;
+  if (cudaMallocAsync((void**)&buf, bytes_a + bytes_b + bytes_s, st) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaMemsetAsync(buf, 0, bytes_a + bytes_b, st);
+  int8_t* sa = buf;
+  int8_t* sb = buf + bytes_a;
+  double* sca = reinterpret_cast<double*>(buf + bytes_a + bytes_b);
+  double* scb = sca + (int64_t)d * m;
+  int tok = prof_begin(PC_OTHER, 0.0, st);
+  auto split = [&](auto kl, const double* src, int64_t ld, int64_t ps, int trans, int64_t R,
+                   int8_t* out, int64_t Rp, int TR, double* sc) {
+    constexpr int KL = decltype(kl)::value;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(split_lines_kernel<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+    split_lines_kernel<KL><<<(unsigned)R, 256, line_smem, st>>>(src, ld, ps, trans, R, n, d, width,
+                                                                shift, out, Rp, Kp, TR, sc);
+  };
+  switch (k) {
+    case 2:
+      split(std::integral_constant<int, 2>{}, A.re, A.ld, A.ps, 0, m, sa, Mp, BM, sca);
+      split(std::integral_constant<int, 2>{}, B.re, B.ld, B.ps, 1, l, sb, Lp, BN, scb);
+      break;
+    case 3:
+      split(std::integral_constant<int, 3>{}, A.re, A.ld, A.ps, 0, m, sa, Mp, BM, sca);
+      split(std::integral_constant<int, 3>{}, B.re, B.ld, B.ps, 1, l, sb, Lp, BN, scb);
+      break;
+    default:
+      split(std::integral_constant<int, 4>{}, A.re, A.ld, A.ps, 0, m, sa, Mp, BM, sca);
+      split(std::integral_constant<int, 4>{}, B.re, B.ld, B.ps, 1, l, sb, Lp, BN, scb);
+      break;
+  }
+  prof_end(tok, st);
+  check_launch("ozaki split_lines_kernel");
+  Params P;
+  memset(&P, 0, sizeof(P));
+  P.sa = sa;
+  P.sb = sb;
+  P.scale_a = sca;
+  P.scale_b = scb;
+  P.m = m;
+  P.l = l;
+  P.Mp = Mp;
+  P.Lp = Lp;
+  P.Kp = Kp;
+  P.npairs = (int)pairs.size();
+  P.shift = shift;
+  P.lo_unsigned = shift == 8 ? 1 : 0;
+  P.C = C;
+  for (size_t i = 0; i < pairs.size(); i++) {
+    P.pp[i] = (unsigned char)pairs[i].first;
+    P.pq[i] = (unsigned char)pairs[i].second;
+  }
   const double ops = 2.0 * NSL * NSL * (double)pairs.size() * (double)m * (double)n * (double)l;
   switch (k) {
     case 2: launch<2>(P, st, ops); break;

@@ -26,6 +26,13 @@ bool ozaki_tc_gemm(int k, int64_t m, int64_t n, int64_t l, const double* parts_a
                    const std::vector<std::pair<int, int>>& pairs, int width, View C,
                    cudaStream_t st);
 
+// rgemm_ozaki (ozaki.py:124-159) end to end on the tensor-core path: the
+// fused split (ozaki_split of A by rows, of B by columns, straight to digit
+// slices) and ozaki_tc_gemm's kernel.  A: m x n, B: n x l, C: m x l views
+// (k planes).  Returns false when outside the supported regime.
+bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View C, int d,
+                    const std::vector<std::pair<int, int>>& pairs, int width, cudaStream_t st);
+
 // MPC_OZAKI_GEMM=dgemm forces the cuBLAS binary64 seam (A/B comparisons)
 bool ozaki_tc_enabled();
 
