@@ -75,7 +75,7 @@ struct Params {
   const double* scale_a;  // [d][m]
   const double* scale_b;  // [d][l]
   int64_t m, l, Mp, Lp, Kp;
-  int npairs, shift, lo_unsigned;
+  int npairs, shift;
   View C;
   unsigned char pp[MAXPAIRS], pq[MAXPAIRS];
 };
@@ -117,6 +117,39 @@ MPC_DI void bulk_g2s(uint32_t sdst, const void* gsrc, uint32_t bytes, uint64_t* 
       : "memory");
 }
 
+// multicast variant: the same smem offset / mbarrier in every CTA of ctaMask
+MPC_DI void bulk_g2s_mc(uint32_t sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                        uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1], %2, [%3], %4;\n" ::"r"(sdst),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+MPC_DI bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+MPC_DI uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+MPC_DI void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+
 MPC_DI void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 MPC_DI void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -155,12 +188,28 @@ MPC_DI void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+MPC_DI void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 MPC_DI void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
                  "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
+MPC_DI void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
+                   taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
+MPC_DI void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 MPC_DI void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // acc_plane insertion of one exact binary64 product (_kernels.py:502-517)
@@ -183,7 +232,7 @@ MPC_DI void acc_insert(Exp<KL>& c, double q) {
 // column half w / 4), warp 8 producer (one lane issues the bulk copies),
 // warp 9 MMA issuer (one lane).  Pipelines: smem ring full/empty (bulk copy
 // -> MMA -> tcgen05.commit), TMEM double buffer full/empty (MMA -> epilogue).
-template <int KL>
+template <int KL, int CN>
 __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant__ Params P) {
   using T = Tile<KL>;
   constexpr int BN = T::BN, S = T::STAGES, HALF = BN / 2;
@@ -199,7 +248,7 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
   if (tid == 0) {
     for (int s = 0; s < S; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CN);  // every CTA of the cluster frees the slot
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&accf[b], 1);
@@ -216,7 +265,9 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (CN > 1) cluster_sync();  // peers' barriers initialised before any multicast
   const uint32_t tmem = tmem_slot;
+  const uint32_t crank = CN > 1 ? cluster_rank() : 0u;
   const uint32_t sbase = smem_u32(smem);
   const int nk = (int)(P.Kp / BKB);
   const int64_t kch = P.Kp / 16;
@@ -229,19 +280,26 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
       uint32_t ph = 0;
       for (int t = 0; t < P.npairs; t++) {
         const int8_t* ga = P.sa + (((int64_t)P.pp[t] * NSL * tilesA + rt) * kch) * (BM * 16);
-        const int8_t* gb = P.sb + (((int64_t)P.pq[t] * NSL * tilesB + ct) * kch) * (BN * 16);
+        // B: the NSL slices of a 16-deep K chunk are stacked (3*BN rows), so
+        // one stage is one contiguous block
+        const int8_t* gb = P.sb + (((int64_t)P.pq[t] * tilesB + ct) * kch) * (NSL * BN * 16);
         for (int kc = 0; kc < nk; kc++) {
           mbar_wait(&empty[slot], ph ^ 1u);
           const uint32_t sA = sbase + (uint32_t)(slot * T::STAGE), sB = sA + T::A_BYTES;
           mbar_expect_tx(&full[slot], (uint32_t)T::STAGE);
+          // the A tile is shared by the cluster (same row tile): CTA r fetches
+          // the r-th 1/CN of each slice and multicasts it to every peer
 #pragma unroll
-          for (int i = 0; i < NSL; i++)
-            bulk_g2s(sA + i * (BM * BKB), ga + ((int64_t)i * tilesA * kch + kc * 4) * (BM * 16),
-                     BM * BKB, &full[slot]);
-#pragma unroll
-          for (int j = 0; j < NSL; j++)
-            bulk_g2s(sB + j * (BN * BKB), gb + ((int64_t)j * tilesB * kch + kc * 4) * (BN * 16),
-                     BN * BKB, &full[slot]);
+          for (int i = 0; i < NSL; i++) {
+            const uint32_t off = crank * (BM * BKB / CN);
+            const int8_t* src = ga + ((int64_t)i * tilesA * kch + kc * 4) * (BM * 16) + off;
+            if constexpr (CN > 1)
+              bulk_g2s_mc(sA + i * (BM * BKB) + off, src, BM * BKB / CN, &full[slot],
+                          (uint16_t)((1u << CN) - 1u));
+            else
+              bulk_g2s(sA + i * (BM * BKB), src, BM * BKB, &full[slot]);
+          }
+          bulk_g2s(sB, gb + (int64_t)kc * 4 * (NSL * BN * 16), T::B_BYTES, &full[slot]);
           if (++slot == S) {
             slot = 0;
             ph ^= 1u;
@@ -250,45 +308,56 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
       }
     }
   } else if (warp == NEPI + 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      int slot = 0;
-      uint32_t ph = 0;
-      for (int t = 0; t < P.npairs; t++) {
-        const int buf = t & 1;
-        mbar_wait(&acce[buf], (uint32_t)(((t >> 1) & 1) ^ 1));  // epilogue drained it
+    // ---------------- MMA issuer: the whole warp walks the pipeline, one
+    // elected lane issues.  Descriptors are precomputed: only the 14-bit
+    // start-address field of the low word moves (smem < 256 KB, no carry).
+    const uint32_t hi = (128u >> 4) | (1u << 14);  // SBO = 128 B, version 1
+    const uint32_t loA = ((uint32_t)(BM * 16) >> 4) << 16,
+                   loB = ((uint32_t)(NSL * BN * 16) >> 4) << 16;
+    // one MMA per A slice against the stacked B slices: N = 3 BN columns,
+    // landing on the consecutive groups i, i+1, i+2 (group g at column g BN)
+    constexpr uint32_t ID = make_idesc(NSL * BN, true, true);
+    const bool leader = elect_one();
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < P.npairs; t++) {
+      const int buf = t & 1;
+      mbar_wait(&acce[buf], (uint32_t)((t >> 1) & 1));  // drained and zeroed
+      tc_fence_after();
+      const uint32_t tacc = tmem + (uint32_t)(buf * 256);
+      for (int kc = 0; kc < nk; kc++) {
+        mbar_wait(&full[slot], ph);
         tc_fence_after();
-        const uint32_t tacc = tmem + (uint32_t)(buf * 256);
-        for (int kc = 0; kc < nk; kc++) {
-          mbar_wait(&full[slot], ph);
-          tc_fence_after();
-          const uint32_t sA = sbase + (uint32_t)(slot * T::STAGE), sB = sA + T::A_BYTES;
+        const uint32_t sA = sbase + (uint32_t)(slot * T::STAGE), sB = sA + T::A_BYTES;
+        // (the shared::cta window address carries the cluster rank above bit 18;
+        // the descriptor takes the 14-bit CTA-local offset)
+        const uint32_t a0 = loA | ((sA >> 4) & 0x3FFFu), b0 = loB | ((sB >> 4) & 0x3FFFu);
+        if (leader) {
 #pragma unroll
           for (int ks = 0; ks < BKB / 32; ks++) {
+            const uint64_t bd =
+                ((uint64_t)hi << 32) | (b0 + (uint32_t)((ks * 2 * (NSL * BN * 16)) >> 4));
 #pragma unroll
             for (int i = 0; i < NSL; i++) {
-#pragma unroll
-              for (int j = 0; j < NSL; j++) {
-                const uint64_t ad =
-                    make_desc(sA + i * (BM * BKB) + ks * 2 * (BM * 16), BM * 16, 128);
-                const uint64_t bd =
-                    make_desc(sB + j * (BN * BKB) + ks * 2 * (BN * 16), BN * 16, 128);
-                // first write into group i + j of this pair: (0,0) (0,1) (0,2) (1,2) (2,2)
-                const uint32_t accum = (kc == 0 && ks == 0 && (i == 0 || j == NSL - 1)) ? 0u : 1u;
-                const uint32_t id =
-                    make_idesc(BN, i == 0 || !P.lo_unsigned, j == 0 || !P.lo_unsigned);
-                mma_i8(tacc + (uint32_t)((i + j) * BN), ad, bd, id, accum);
-              }
+              const uint64_t ad =
+                  ((uint64_t)hi << 32) | (a0 + (uint32_t)((i * (BM * BKB) + ks * 2 * (BM * 16)) >> 4));
+              mma_i8(tacc + (uint32_t)(i * BN), ad, bd, ID, 1u);
             }
           }
-          mma_commit(&empty[slot]);  // slot free once these MMAs have read it
-          if (++slot == S) {
-            slot = 0;
-            ph ^= 1u;
-          }
+          // slot free (in every CTA of the cluster) once these MMAs have read it
+          if constexpr (CN > 1)
+            mma_commit_mc(&empty[slot], (uint16_t)((1u << CN) - 1u));
+          else
+            mma_commit(&empty[slot]);
         }
-        mma_commit(&accf[buf]);  // accumulators of pair t complete
+        __syncwarp();
+        if (++slot == S) {
+          slot = 0;
+          ph ^= 1u;
+        }
       }
+      if (leader) mma_commit(&accf[buf]);  // accumulators of pair t complete
+      __syncwarp();
     }
   } else {
     // ---------------- epilogue: J = sum_s 2^(b(4-s)) G_s, P = J 2^ea 2^eb, acc_plane
@@ -299,6 +368,19 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
 #pragma unroll
     for (int j = 0; j < HALF; j++) acc[j] = exp_zero<KL>();
     const int b = P.shift;
+    // zero this thread's accumulator columns of both buffers (the MMAs always
+    // accumulate), then hand the buffers to the MMA warp
+    const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)cbase;
+    uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    for (int bb = 0; bb < 2; bb++) {
+#pragma unroll
+      for (int g = 0; g < NGRP; g++)
+#pragma unroll
+        for (int cc = 0; cc < HALF / 8; cc++) tmem_st8(tq + (uint32_t)(bb * 256 + g * BN + cc * 8), z);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&acce[bb]);
+    }
     for (int t = 0; t < P.npairs; t++) {
       const int buf = t & 1;
       mbar_wait(&accf[buf], (uint32_t)((t >> 1) & 1));
@@ -312,9 +394,12 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
 #pragma unroll
         for (int g = 0; g < NGRP; g++) tmem_ld8(trow + (uint32_t)(g * BN + cc * 8), r[g]);
         tmem_wait_ld();
+#pragma unroll
+        for (int g = 0; g < NGRP; g++) tmem_st8(trow + (uint32_t)(g * BN + cc * 8), z);
         if (cc == HALF / 8 - 1) {
+          tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&acce[buf]);  // this thread's TMEM reads of pair t are done
+          mbar_arrive(&acce[buf]);  // drained and re-zeroed for pair t + 2
         }
 #pragma unroll
         for (int jj = 0; jj < 8; jj++) {
@@ -345,53 +430,11 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CN > 1) cluster_sync();  // no peer still signals / writes into this CTA
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "r"(TCOLS));
-  }
-}
-
-// part (row-major, ld) -> NSL digit slices in the stage-contiguous tiled
-// layout [s][R/TR][Kp/16][TR][16] (TR = BM for the left operand, BN for the
-// right one):
-// side 0 (left):  element (i, t) from part[i][t] / scale[i]   (R = rows, Kd = cols)
-// side 1 (right): element (j, t) from part[t][j] / scale[j]   (R = cols, Kd = rows)
-// one thread per (r, 16-deep group of t); the buffer was zeroed beforehand
-__global__ void slice_kernel(const double* part, int64_t rows, int64_t cols, int64_t ld,
-                             const double* scale, int side, int shift, int8_t* out, int64_t Rp,
-                             int64_t Kp, int TR) {
-  const int64_t R = side == 0 ? rows : cols, Kd = side == 0 ? cols : rows;
-  const int64_t ng = (Kd + 15) / 16;
-  const int64_t mask = (1ll << shift) - 1;
-  const int64_t kch = Kp / 16, slice = Rp * Kp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < R * ng;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = side == 0 ? e / ng : e % R;
-    const int64_t g = side == 0 ? e % ng : e / R;
-    int es = 0;
-    frexp(scale[r], &es);
-    es -= 1;  // scale = 2^es (a power of two by construction, ozaki.py:107)
-    union {
-      int8_t b[16];
-      int4 v;
-    } d0, d1, d2;
-#pragma unroll
-    for (int tt = 0; tt < 16; tt++) {
-      const int64_t t = g * 16 + tt;
-      long long I = 0;
-      if (t < Kd) {
-        const double x = side == 0 ? part[r * ld + t] : part[t * ld + r];
-        I = __double2ll_rn(ldexp(x, -es));  // exact: x is an integer multiple of 2^es
-      }
-      d0.b[tt] = (int8_t)(I >> (2 * shift));
-      d1.b[tt] = (int8_t)(uint8_t)((I >> shift) & mask);
-      d2.b[tt] = (int8_t)(uint8_t)(I & mask);
-    }
-    int8_t* o = out + ((r / TR) * kch + g) * (TR * 16) + (r % TR) * 16;
-    *reinterpret_cast<int4*>(o) = d0.v;
-    *reinterpret_cast<int4*>(o + slice) = d1.v;
-    *reinterpret_cast<int4*>(o + 2 * slice) = d2.v;
   }
 }
 
@@ -410,7 +453,7 @@ __global__ void __launch_bounds__(256) split_lines_kernel(const double* src, int
                                                           int trans, int64_t R, int64_t n, int d,
                                                           int width, int shift, int8_t* out,
                                                           int64_t Rp, int64_t Kp, int TR,
-                                                          double* scale) {
+                                                          int stackB, double* scale) {
   extern __shared__ double res[];  // [KL][n]
   __shared__ double red[8];
   const int64_t r = blockIdx.x;
@@ -421,7 +464,7 @@ __global__ void __launch_bounds__(256) split_lines_kernel(const double* src, int
       res[c * n + t] = trans ? src[c * ps + t * ld + r] : src[c * ps + r * ld + t];
   __syncthreads();
   const int64_t kch = Kp / 16, slice = Rp * Kp;
-  const int64_t mask = (1ll << shift) - 1;
+  const long long mask = (1ll << shift) - 1, half = 1ll << (shift - 1);
   const double shiftS = ldexp(1.0, 53 - width);
   for (int p = 0; p < d; p++) {
     double m = 0.0;
@@ -440,7 +483,11 @@ __global__ void __launch_bounds__(256) split_lines_kernel(const double* src, int
     const double S = __dmul_rn(w, shiftS);
     const int es = ex - width;  // scale = ldexp(w, -width) = 2^es
     if (tid == 0) scale[(int64_t)p * R + r] = ldexp(w, -width);
-    int8_t* o = out + (int64_t)p * NSL * slice + ((r / TR) * kch) * (TR * 16) + (r % TR) * 16;
+    // left (stackB = 0): [p][s][R/TR][kch][TR][16]; right (stackB = 1):
+    // [p][R/TR][kch][s][TR][16] (the three slices of a K chunk stacked)
+    const int64_t sstride = stackB ? (int64_t)TR * 16 : slice;
+    const int64_t gstride = stackB ? (int64_t)NSL * TR * 16 : (int64_t)TR * 16;
+    int8_t* o = out + (int64_t)p * NSL * slice + ((r / TR) * kch) * gstride + (r % TR) * 16;
     for (int64_t g = tid; g < (n + 15) / 16; g += blockDim.x) {
       union {
         int8_t b[16];
@@ -462,14 +509,19 @@ __global__ void __launch_bounds__(256) split_lines_kernel(const double* src, int
           for (int c = 0; c < KL; c++) res[c * n + t] = e.c[c];
           I = __double2ll_rn(ldexp(pt, -es));  // exact: pt is a multiple of 2^es
         }
-        d0.b[tt] = (int8_t)(I >> (2 * shift));
-        d1.b[tt] = (int8_t)(uint8_t)((I >> shift) & mask);
-        d2.b[tt] = (int8_t)(uint8_t)(I & mask);
+        // balanced signed digits: I = a0 2^(2b) + a1 2^b + a2, a1, a2 in
+        // [-2^(b-1), 2^(b-1)), |a0| <= 2^(w-2b) + 1 -- all s8
+        const long long a2 = ((I + half) & mask) - half;
+        const long long I1 = (I - a2) >> shift;
+        const long long a1 = ((I1 + half) & mask) - half;
+        d0.b[tt] = (int8_t)((I1 - a1) >> shift);
+        d1.b[tt] = (int8_t)a1;
+        d2.b[tt] = (int8_t)a2;
       }
-      int8_t* og = o + g * (TR * 16);
+      int8_t* og = o + g * gstride;
       *reinterpret_cast<int4*>(og) = d0.v;
-      *reinterpret_cast<int4*>(og + slice) = d1.v;
-      *reinterpret_cast<int4*>(og + 2 * slice) = d2.v;
+      *reinterpret_cast<int4*>(og + sstride) = d1.v;
+      *reinterpret_cast<int4*>(og + 2 * sstride) = d2.v;
     }
     __syncthreads();
   }
@@ -480,19 +532,50 @@ unsigned grid_for(int64_t total) {
   return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
 }
 
-template <int KL>
-void launch(const Params& P, cudaStream_t st, double ops) {
+template <int KL, int CN>
+void launch_cn(const Params& P, cudaStream_t st, double ops) {
   using T = Tile<KL>;
   static bool attr = false;
+  auto kern = ozaki_tc_kernel<KL, CN>;
   if (!attr) {
-    cudaFuncSetAttribute(ozaki_tc_kernel<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
     attr = true;
   }
-  dim3 grid((unsigned)(P.Lp / T::BN), (unsigned)(P.Mp / BM));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P.Lp / T::BN), (unsigned)(P.Mp / BM));
+  cfg.blockDim = dim3(NTHR);
+  cfg.dynamicSmemBytes = T::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CN;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
   int tok = prof_begin(PC_GEMM, ops, st);
-  ozaki_tc_kernel<KL><<<grid, NTHR, T::SMEM, st>>>(P);
+  cudaLaunchKernelEx(&cfg, kern, P);
   prof_end(tok, st);
   check_launch("ozaki_tc_kernel");
+}
+
+// cluster size along the column tiles (A-tile multicast), MPC_OZAKI_CLUSTER
+inline int cluster_n() {
+  static int cn = [] {
+    const char* e = getenv("MPC_OZAKI_CLUSTER");
+    int v = e ? atoi(e) : 4;
+    return (v == 1 || v == 2 || v == 4) ? v : 4;
+  }();
+  return cn;
+}
+
+template <int KL>
+void launch(const Params& P, cudaStream_t st, double ops) {
+  switch (cluster_n()) {
+    case 1: launch_cn<KL, 1>(P, st, ops); break;
+    case 2: launch_cn<KL, 2>(P, st, ops); break;
+    default: launch_cn<KL, 4>(P, st, ops); break;
+  }
 }
 
 }  // namespace otc
@@ -500,79 +583,6 @@ void launch(const Params& P, cudaStream_t st, double ops) {
 bool ozaki_tc_enabled() {
   const char* e = getenv("MPC_OZAKI_GEMM");
   return !(e && strcmp(e, "dgemm") == 0);
-}
-
-bool ozaki_tc_gemm(int k, int64_t m, int64_t n, int64_t l, const double* parts_a,
-                   const double* parts_b, const double* scale_a, const double* scale_b, int d,
-                   const std::vector<std::pair<int, int>>& pairs, int width, View C,
-                   cudaStream_t st) {
-  using namespace otc;
-  if (k < 2 || k > 4 || m <= 0 || l <= 0 || n <= 0) return false;
-  if ((int)pairs.size() > MAXPAIRS || d > 255) return false;
-  // digit base and the int32 headroom of the largest accumulator group
-  int shift;
-  double gmax;
-  if (width <= 20) {
-    shift = 7;       // |a0| <= 2^20 / 2^14 = 64, a1, a2 in [0, 127]: all s8
-    gmax = 32385.0;  // 64*127 + 127*127 + 127*64
-  } else if (width <= 22) {
-    shift = 8;        // |a0| <= 64 (s8), a1, a2 in [0, 255] (u8)
-    gmax = 130050.0;  // 255*255*2
-  } else {
-    return false;
-  }
-  if (gmax * (double)n >= 2147483648.0) return false;
-  const int BN = k == 2 ? Tile<2>::BN : Tile<3>::BN;
-  const int64_t Mp = (m + BM - 1) / BM * BM, Lp = (l + BN - 1) / BN * BN,
-                Kp = (n + BKB - 1) / BKB * BKB;
-  const size_t bytes_a = (size_t)d * NSL * Mp * Kp, bytes_b = (size_t)d * NSL * Lp * Kp;
-  int8_t* buf = nullptr;
-  if (cudaMallocAsync((void**)&buf, bytes_a + bytes_b, st) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  cudaMemsetAsync(buf, 0, bytes_a + bytes_b, st);
-  int8_t* sa = buf;
-  int8_t* sb = buf + bytes_a;
-  int tok = prof_begin(PC_OTHER, 0.0, st);
-  for (int p = 0; p < d; p++) {
-    slice_kernel<<<grid_for(m * ((n + 15) / 16)), 256, 0, st>>>(
-        parts_a + (int64_t)p * m * n, m, n, n, scale_a + (int64_t)p * m, 0, shift,
-        sa + (int64_t)p * NSL * Mp * Kp, Mp, Kp, BM);
-    slice_kernel<<<grid_for(l * ((n + 15) / 16)), 256, 0, st>>>(
-        parts_b + (int64_t)p * n * l, n, l, l, scale_b + (int64_t)p * l, 1, shift,
-        sb + (int64_t)p * NSL * Lp * Kp, Lp, Kp, BN);
-  }
-  prof_end(tok, st);
-  check_launch("ozaki slice_kernel");
-  Params P;
-  memset(&P, 0, sizeof(P));
-  P.sa = sa;
-  P.sb = sb;
-  P.scale_a = scale_a;
-  P.scale_b = scale_b;
-  P.m = m;
-  P.l = l;
-  P.Mp = Mp;
-  P.Lp = Lp;
-  P.Kp = Kp;
-  P.npairs = (int)pairs.size();
-  P.shift = shift;
-  P.lo_unsigned = shift == 8 ? 1 : 0;
-  P.C = C;
-  for (size_t i = 0; i < pairs.size(); i++) {
-    P.pp[i] = (unsigned char)pairs[i].first;
-    P.pq[i] = (unsigned char)pairs[i].second;
-  }
-  // INT8 tensor-core ops issued (2 per MAC, NSL^2 slice products per pair)
-  const double ops = 2.0 * NSL * NSL * (double)pairs.size() * (double)m * (double)n * (double)l;
-  switch (k) {
-    case 2: launch<2>(P, st, ops); break;
-    case 3: launch<3>(P, st, ops); break;
-    default: launch<4>(P, st, ops); break;
-  }
-  cudaFreeAsync(buf, st);
-  return true;
 }
 
 bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View C, int d,
@@ -584,10 +594,10 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
   double gmax;
   if (width <= 20) {
     shift = 7;
-    gmax = 32385.0;
+    gmax = 12416.0;  // largest |G_s| term per k: 65*64*2 + 64*64
   } else if (width <= 22) {
     shift = 8;
-    gmax = 130050.0;
+    gmax = 33024.0;  // 65*128*2 + 128*128
   } else {
     return false;
   }
@@ -595,7 +605,8 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
   const size_t line_smem = sizeof(double) * (size_t)k * (size_t)n;
   if (line_smem > 200 * 1024) return false;
   const int BN = k == 2 ? Tile<2>::BN : Tile<3>::BN;
-  const int64_t Mp = (m + BM - 1) / BM * BM, Lp = (l + BN - 1) / BN * BN,
+  const int64_t LT = (int64_t)BN * cluster_n();  // column tiles come in whole clusters
+  const int64_t Mp = (m + BM - 1) / BM * BM, Lp = (l + LT - 1) / LT * LT,
                 Kp = (n + BKB - 1) / BKB * BKB;
   const size_t bytes_a = (size_t)d * NSL * Mp * Kp, bytes_b = (size_t)d * NSL * Lp * Kp;
   const size_t bytes_s = sizeof(double) * (size_t)d * (size_t)(m + l);
@@ -612,6 +623,7 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
   int tok = prof_begin(PC_OTHER, 0.0, st);
   auto split = [&](auto kl, const double* src, int64_t ld, int64_t ps, int trans, int64_t R,
                    int8_t* out, int64_t Rp, int TR, double* sc) {
+    const int stackB = trans;  // right operand: slices stacked per K chunk
     constexpr int KL = decltype(kl)::value;
     static bool attr = false;
     if (!attr) {
@@ -620,7 +632,7 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
       attr = true;
     }
     split_lines_kernel<KL><<<(unsigned)R, 256, line_smem, st>>>(src, ld, ps, trans, R, n, d, width,
-                                                                shift, out, Rp, Kp, TR, sc);
+                                                                shift, out, Rp, Kp, TR, stackB, sc);
   };
   switch (k) {
     case 2:
@@ -651,7 +663,6 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
   P.Kp = Kp;
   P.npairs = (int)pairs.size();
   P.shift = shift;
-  P.lo_unsigned = shift == 8 ? 1 : 0;
   P.C = C;
   for (size_t i = 0; i < pairs.size(); i++) {
     P.pp[i] = (unsigned char)pairs[i].first;
