@@ -47,6 +47,10 @@ def parse():
     p.add_argument("--K", type=int, default=512)
     p.add_argument("--k", type=int, default=2)
     p.add_argument("--method", default="3m", choices=["3m", "4m"])
+    p.add_argument("--real-kernel", default="blocked", choices=["blocked", "ozaki"],
+                   help="trailing-update real kernel (KernelChoice.real_kernel): the EFT "
+                        "FP64 GEMM (default, the reference's default) or the Ozaki scheme "
+                        "on the INT8 tensor cores")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--ill", action="store_true", help="row-scaled ill-conditioned input (cfg4 #2)")
     p.add_argument("--no-e2e", action="store_true")
@@ -64,8 +68,11 @@ def workload(args):
     prec = {2: "DD", 3: "TD", 4: "QD"}[args.k]
     tag = {(16384, 512, 2): "cfg4", (4096, 256, 2): "cfg2", (128, 128, 2): "cfg0",
            (2048, 128, 3): "cfg3", (2048, 128, 4): "cfg3"}.get((args.n, args.K, args.k), "custom")
+    rk = getattr(args, "real_kernel", "blocked")
     return (f"{tag}: complex {prec} blocked LU with partial pivoting, n={args.n}, K={args.K}, "
-            f"{args.method.upper()} trailing update" + (", ill-conditioned rows" if args.ill else ""))
+            f"{args.method.upper()} trailing update" + (", ill-conditioned rows" if args.ill else "")
+            + (", real_kernel=ozaki (d=%d, INT8 tensor cores)" % {2: 6, 3: 8, 4: 12}[args.k]
+               if rk == "ozaki" else ""))
 
 
 # ------------------------------------------------------------------ clocks
@@ -205,10 +212,15 @@ def run_b200(args, rank, world):
     piv = torch.empty(n, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    ozaki = args.real_kernel == "ozaki"
+
     def step():
         Wr.copy_(A0r)
         Wi.copy_(A0i)
-        st = device.getrf(Wr, Wi, piv, K, args.method)
+        if ozaki:
+            st = device.getrf_ozaki(Wr, Wi, piv, K, args.method)
+        else:
+            st = device.getrf(Wr, Wi, piv, K, args.method)
         if st != -1:
             raise RuntimeError(f"singular at column {st}")
 
@@ -216,6 +228,7 @@ def run_b200(args, rank, world):
         step()
     torch.cuda.synchronize()
     peak = device.fp64_peak()  # lane-ops/s, measured now on this device
+    peak_i8 = device.int8_peak() if ozaki else None
     if not args.no_prof:
         # event-time only the dominant kernel inside the timed region (cheap:
         # a few launches per step); the full per-class breakdown comes from
@@ -252,19 +265,31 @@ def run_b200(args, rank, world):
     total_ops = None
     if prof:
         g_ms, g_ops, g_cnt = prof["gemm"]
-        achieved = g_ops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
-        peak_t = peak / 1e12
-        roof = {"bound": "fp64", "achieved": achieved, "peak": peak_t,
-                "unit": "TFLOP/s (FP64 instr/s, DADD/DMUL/DFMA = 1)", "frac": achieved / peak_t,
-                "traffic": None, "kernel": "gemm_kernel<K=2,MODE_G3> (fused 3M trailing update)",
-                "launches": g_cnt, "avg_launch_ms": g_ms / max(g_cnt, 1),
-                "peak_source": "measured DADD microbenchmark (mpc_fp64_peak) on this device, "
-                               "this run; nominal 18.6 T/s at 1965 MHz"}
-        breakdown = {c: {"ms": v[0], "fp64_ops": v[1], "launches": v[2]}
+        if ozaki:
+            achieved = g_ops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+            peak_t = peak_i8 / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak_t,
+                    "unit": "TOP/s (INT8 tensor-core ops, 2 per MAC)", "frac": achieved / peak_t,
+                    "traffic": None,
+                    "kernel": "ozaki_tc_kernel (tcgen05.mma kind::i8, fused acc_plane + renorm)",
+                    "launches": g_cnt, "avg_launch_ms": g_ms / max(g_cnt, 1),
+                    "peak_source": "measured tcgen05 kind::i8 M128 N256 issue-rate microbenchmark "
+                                   "(mpc_int8_peak) on this device, this run; nominal 4.5 POPS"}
+        else:
+            achieved = g_ops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+            peak_t = peak / 1e12
+            roof = {"bound": "fp64", "achieved": achieved, "peak": peak_t,
+                    "unit": "TFLOP/s (FP64 instr/s, DADD/DMUL/DFMA = 1)", "frac": achieved / peak_t,
+                    "traffic": None, "kernel": "gemm_kernel<K=2,MODE_G3> (fused 3M trailing update)",
+                    "launches": g_cnt, "avg_launch_ms": g_ms / max(g_cnt, 1),
+                    "peak_source": "measured DADD microbenchmark (mpc_fp64_peak) on this device, "
+                                   "this run; nominal 18.6 T/s at 1965 MHz"}
+        breakdown = {c: {"ms": v[0], "ops": v[1], "launches": v[2]}
                      for c, v in full.items()}
         breakdown["note"] = ("one extra step with every launch event-timed (adds launch "
-                             "overhead); per-class kernel time, not wall time")
-        total_ops = sum(v[1] for v in full.values())
+                             "overhead); per-class kernel time, not wall time; ops are FP64 "
+                             "instructions except the ozaki gemm class (INT8 tensor-core ops)")
+        total_ops = sum(v[1] for c, v in full.items() if not (ozaki and c == "gemm"))
     fp64_pct = (100.0 * total_ops / (ms_step * 1e-3) / peak) if total_ops else None
 
     # e2e: public in-place API on pinned host buffers (H2D + factor + D2H)
@@ -281,7 +306,8 @@ def run_b200(args, rank, world):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(torch.cuda.default_stream(dev))
-            mp.lu.factor_inplace(hr.numpy(), hi.numpy(), K, args.method, piv=hp.numpy())
+            mp.lu.factor_inplace(hr.numpy(), hi.numpy(), K, args.method, piv=hp.numpy(),
+                                 real_kernel=args.real_kernel)
             e1.record(torch.cuda.default_stream(dev))
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -292,7 +318,8 @@ def run_b200(args, rank, world):
                "h2d_bytes_per_step": int(re0.nbytes + im0.nbytes),
                "d2h_bytes_per_step": int(re0.nbytes + im0.nbytes + 8 * n),
                "ms_per_step": t, "steps": len(times), "pivots_match_device_run": same,
-               "api": "paper_2403_16013_b200.lu.factor_inplace (mpc_getrf, host pointers)"}
+               "api": "paper_2403_16013_b200.lu.factor_inplace (%s, host pointers)"
+                      % ("mpc_getrf_ozaki" if ozaki else "mpc_getrf")}
 
     cpu = None
     if not args.no_cpu:
@@ -311,6 +338,7 @@ def run_b200(args, rank, world):
                    "seed": args.seed, "parallelism": "1 GPU",
                    "l2": "inputs 8 GiB > 126 MB L2, restored from a pristine copy every step"},
         "fp64_pct_of_measured_peak": fp64_pct,
+        "int8_peak_measured_tops": peak_i8 / 1e12 if peak_i8 else None,
         "fp64_peak_measured_tops": peak / 1e12,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
         "gpu_launches": int(launches), "breakdown": breakdown,

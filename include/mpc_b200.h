@@ -169,6 +169,11 @@ long long mpc_launch_count(void);
 /* Measured FP64 (DADD) issue rate of the current device, lane-ops/s. */
 double mpc_fp64_peak(int iters, void* stream);
 
+/* Measured INT8 tensor-core rate of the current device (tcgen05.mma
+ * kind::i8 M=128 N=256 K=32 back to back on every SM; ops/s, 2 per MAC):
+ * the roofline denominator of the Ozaki tensor-core kernel. */
+double mpc_int8_peak(int iters, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,7 @@ _SIGS = {
     "mpc_prof_summary": (_i, [_p, _p, _p, _i]),
     "mpc_launch_count": (ctypes.c_longlong, []),
     "mpc_fp64_peak": (_d, [_i, _p]),
+    "mpc_int8_peak": (_d, [_i, _p]),
 }
 
 PROF_CLASSES = ("gemm", "supdate", "panel", "trsm_diag", "laswp", "other")

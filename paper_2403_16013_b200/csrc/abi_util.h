@@ -92,6 +92,7 @@ class Stager {
   T* map(T* p, int64_t nelem, bool in, bool out) {
     if (!host_ || p == nullptr || nelem <= 0) return p;
     Region r{(void*)p, (size_t)nelem * sizeof(T), out, nullptr};
+    mpc::retain_pool();
     ck(cudaMallocAsync(&r.dev, r.bytes, st_), "cudaMallocAsync");
     regs_.push_back(r);
     if (in) ck(cudaMemcpyAsync(r.dev, p, r.bytes, cudaMemcpyHostToDevice, st_), "H2D");
@@ -126,6 +127,7 @@ struct WsHolder {
   WsHolder(int k, int64_t n, cudaStream_t s) : st(s) {
     int64_t nb = (n + mpc::PNT - 1) / mpc::PNT + 1;
     size_t bytes = sizeof(double) * nb * k + sizeof(int64_t) * nb + 64;
+    mpc::retain_pool();
     ck(cudaMallocAsync(&mem, bytes, st), "cudaMallocAsync(ws)");
     char* b = (char*)mem;
     ws.status = (int64_t*)b;

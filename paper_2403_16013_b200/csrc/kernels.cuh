@@ -891,6 +891,21 @@ inline void check_launch(const char* what) {
   if (e != cudaSuccess) throw LaunchError{what};
 }
 
+// Stream-ordered temporaries (cudaMallocAsync) come from the device's default
+// pool; keep freed blocks in the pool instead of returning them to the OS at
+// every synchronisation, so per-call workspaces cost no page mapping.
+inline void retain_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 inline unsigned cdiv_u(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 template <int K>

@@ -193,6 +193,7 @@ struct DevBuf {
   void* p = nullptr;
   cudaStream_t st;
   DevBuf(size_t bytes, cudaStream_t s) : st(s) {
+    retain_pool();
     if (bytes) ck(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
   }
   ~DevBuf() {
@@ -458,21 +459,49 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
     bool use3m = method == 3;
     mpc::View A{dr, di, n, n * n};
     WsHolder w(k, n, st);
-    std::vector<int64_t> steps;
+    if (mpc::resolve_width(k, std::min(K, n), split_bits) < 0)
+      return fail("dimension exceeds split exactness budget");
+    // Same schedule as mpc_getrf (depth-1 lookahead): the narrow update of
+    // block b+1, its panel factorization on a high-priority side stream, the
+    // rest of block b's update overlapping it.  Column ranges of the Ozaki
+    // update are independent (right-operand grids are per column, left-
+    // operand grids per row of L21), so the split schedule is bit-identical
+    // to lu.py's sequential one.  A singular panel sets the device status;
+    // later panels early-out and the status is read once at the end (the
+    // reference raises at the first singular column, lu.py:139-141).
+    auto update_cols = [&](int64_t jb, int64_t kw, int64_t c0, int64_t c1, cudaStream_t s) {
+      if (c1 <= c0) return;
+      int64_t end = jb + kw;
+      T->laswp(A, c0, c1 - c0, dp, jb, end, s, w.ws.status);
+      T->trsm(use3m, kw, c1 - c0, A.sub(jb, jb), A.sub(jb, c0), s, w.ws.status);
+      mpc::cgemm_ozaki_dev(k, use3m, n - end, kw, c1 - c0, A.sub(end, jb), A.sub(jb, c0),
+                           A.sub(end, c0), 1, d, mpc::resolve_width(k, kw, split_bits), s);
+    };
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStream_t sp;
+    cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi);
+    cudaEvent_t ev_narrow, ev_panel;
+    cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+    T->panel_rec(use3m, A, n, 0, std::min(K, n), dp, w.ws, st);
     for (int64_t jb = 0; jb < n; jb += K) {
       int64_t kw = std::min(K, n - jb);
-      T->lu_panel(use3m, A, n, jb, kw, dp, w.ws, st);
       int64_t end = jb + kw;
+      T->laswp(A, 0, jb, dp, jb, end, st, w.ws.status);  // left of the panel
       if (end == n) break;
-      int64_t M = n - end;
-      T->trsm(use3m, kw, M, A.sub(jb, jb), A.sub(jb, end), st, w.ws.status);
-      int width = mpc::resolve_width(k, kw, split_bits);
-      if (width < 0) return fail("dimension exceeds split exactness budget");
-      // the reference raises at the first singular panel; check before updating
-      if (w.read_status() >= 0) break;
-      mpc::cgemm_ozaki_dev(k, use3m, M, kw, M, A.sub(end, jb), A.sub(jb, end), A.sub(end, end), 1,
-                           d, width, st);
+      int64_t kw2 = std::min(K, n - end);
+      update_cols(jb, kw, end, end + kw2, st);
+      cudaEventRecord(ev_narrow, st);
+      cudaStreamWaitEvent(sp, ev_narrow, 0);
+      T->panel_rec(use3m, A, n, end, kw2, dp, w.ws, sp);
+      cudaEventRecord(ev_panel, sp);
+      update_cols(jb, kw, end + kw2, n, st);
+      cudaStreamWaitEvent(st, ev_panel, 0);
     }
+    cudaEventDestroy(ev_narrow);
+    cudaEventDestroy(ev_panel);
+    cudaStreamDestroy(sp);
     status = w.read_status();
   }
   sg.finish();

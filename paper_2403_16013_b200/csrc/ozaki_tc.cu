@@ -578,6 +578,55 @@ void launch(const Params& P, cudaStream_t st, double ops) {
   }
 }
 
+// INT8 tensor-core issue-rate microbenchmark (the roofline denominator of
+// the Ozaki kernel): one CTA per SM, one thread issuing back-to-back
+// tcgen05.mma.kind::i8 M=128 N=256 K=32 from a resident 12 KB smem tile into
+// two TMEM accumulators; int8 ops = 2 * 128 * 256 * 32 per MMA.
+__global__ void __launch_bounds__(128, 1) int8_peak_kernel(int iters, int* sink) {
+  __shared__ __align__(128) int8_t tile[BM * 32 + 256 * 32];
+  __shared__ __align__(8) uint64_t done;
+  __shared__ uint32_t tmem_slot;
+  for (int i = threadIdx.x; i < (BM * 32 + 256 * 32) / 4; i += blockDim.x)
+    reinterpret_cast<int*>(tile)[i] = 0x01010101 * (i & 3);
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  if (threadIdx.x < 32) {
+    const uint32_t s = smem_u32(tile);
+    const uint32_t hi = (128u >> 4) | (1u << 14);
+    const uint64_t ad = ((uint64_t)hi << 32) | (((uint32_t)(BM * 16) >> 4) << 16) | ((s >> 4) & 0x3FFFu);
+    const uint64_t bd = ((uint64_t)hi << 32) | (((uint32_t)(256 * 16) >> 4) << 16) |
+                        (((s + BM * 32) >> 4) & 0x3FFFu);
+    constexpr uint32_t ID = make_idesc(256, true, true);
+    if (elect_one()) {
+      for (int it = 0; it < iters; it++) mma_i8(tmem + (uint32_t)((it & 1) * 256), ad, bd, ID, 1u);
+      mma_commit(&done);
+    }
+    __syncwarp();
+    mbar_wait(&done, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    if (threadIdx.x == 0 && iters < 0) sink[0] = (int)tmem;
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(TCOLS));
+  }
+}
+
 }  // namespace otc
 
 bool ozaki_tc_enabled() {
@@ -611,6 +660,7 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
   const size_t bytes_a = (size_t)d * NSL * Mp * Kp, bytes_b = (size_t)d * NSL * Lp * Kp;
   const size_t bytes_s = sizeof(double) * (size_t)d * (size_t)(m + l);
   int8_t* buf = nullptr;
+  retain_pool();
   if (cudaMallocAsync((void**)&buf, bytes_a + bytes_b + bytes_s, st) != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -679,3 +729,25 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
 }
 
 }  // namespace mpc
+
+extern "C" double mpc_int8_peak(int iters, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  mpc::otc::int8_peak_kernel<<<sms, 128, 0, st>>>(iters / 10 + 1, nullptr);  // warm-up
+  cudaEventRecord(a, st);
+  mpc::otc::int8_peak_kernel<<<sms, 128, 0, st>>>(iters, nullptr);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float t = 0.f;
+  cudaEventElapsedTime(&t, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (cudaGetLastError() != cudaSuccess || t <= 0.f) return -1.0;
+  const double ops = (double)sms * (double)iters * 2.0 * mpc::otc::BM * 256.0 * 32.0;
+  return ops / (t * 1e-3);  // INT8 tensor-core ops per second
+}

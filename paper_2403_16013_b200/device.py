@@ -30,6 +30,11 @@ def getrf(re, im, piv, K, method="3m"):
                                            im.data_ptr(), piv.data_ptr(), _stream(re)), "getrf")
 
 
+def int8_peak(iters=200000):
+    """Measured INT8 tensor-core rate of the current device (ops/s)."""
+    return float(_lib.lib().mpc_int8_peak(iters, torch.cuda.current_stream().cuda_stream))
+
+
 def fp64_peak(iters=20000):
     """Measured FP64 issue rate of the current device (lane-ops/s)."""
     return float(_lib.lib().mpc_fp64_peak(iters, torch.cuda.current_stream().cuda_stream))

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .cmatrix import KernelChoice, PlanarComplexMatrix, _check_k
+from .cmatrix import DEFAULT_SPLITS, KernelChoice, PlanarComplexMatrix, _check_k
 from .rmatrix import RealMatrix, check_threads
 
 
@@ -223,7 +223,8 @@ def max_rel_err(xhat, x):
     return float(np.max(np.hypot(dr, di) / den)) if x.n else 0.0
 
 
-def factor_inplace(re, im, K, method="3m", piv=None):
+def factor_inplace(re, im, K, method="3m", piv=None, real_kernel="blocked", d=None,
+                   split_bits=None):
     """In-place variant of lu_blocked on raw planar buffers (no copies):
     ``re``/``im`` are (k, n, n) float64 C-contiguous numpy arrays (pinned or
     pageable host memory, staged by the C-ABI) or CUDA tensors (device
@@ -240,8 +241,14 @@ def factor_inplace(re, im, K, method="3m", piv=None):
         import torch
 
         stream = torch.cuda.current_stream(re.device).cuda_stream
-    st = _lib.check(_lib.lib().mpc_getrf(k, 3 if method == "3m" else 4, n, K, _lib.ptr(re),
-                                         _lib.ptr(im), _lib.ptr(piv), stream), "getrf")
+    if real_kernel == "ozaki":
+        d = d if d is not None else DEFAULT_SPLITS[k]
+        st = _lib.check(_lib.lib().mpc_getrf_ozaki(
+            k, 3 if method == "3m" else 4, n, K, _lib.ptr(re), _lib.ptr(im), _lib.ptr(piv), d,
+            int(split_bits) if split_bits is not None else 0, stream), "getrf_ozaki")
+    else:
+        st = _lib.check(_lib.lib().mpc_getrf(k, 3 if method == "3m" else 4, n, K, _lib.ptr(re),
+                                             _lib.ptr(im), _lib.ptr(piv), stream), "getrf")
     if st >= 0:
         raise SingularMatrixError(int(st))
     return piv
