@@ -244,13 +244,16 @@ int resolve_width(int k, int64_t inner, int split_bits) {
 }
 
 // rgemm_ozaki (ozaki.py:124-159) on device views; C (m x l) receives the result
-void rgemm_ozaki_dev(int k, int64_t m, int64_t n, int64_t l, View A, View B, View C, int d,
-                     int width, cudaStream_t st) {
+// (with cb: returns true iff the tensor-core path also applied the fused
+// complex composition, see OzCombine; C is then untouched)
+bool rgemm_ozaki_dev(int k, int64_t m, int64_t n, int64_t l, View A, View B, View C, int d,
+                     int width, cudaStream_t st, const OzCombine* cb = nullptr) {
   const OpsTable* T = table_for(k);
-  if (m <= 0 || l <= 0) return;
+  if (m <= 0 || l <= 0) return false;
   const auto pairs = pair_schedule(d, width, k);
   // fused split + exact part products on the INT8 tensor cores + acc_plane + renorm
-  if (ozaki_tc_enabled() && ozaki_tc_rgemm(k, m, n, l, A, B, C, d, pairs, width, st)) return;
+  if (ozaki_tc_enabled() && ozaki_tc_rgemm(k, m, n, l, A, B, C, d, pairs, width, st, cb))
+    return cb != nullptr;
   DevBuf ra(sizeof(double) * k * m * n, st), rb(sizeof(double) * k * n * l, st);
   DevBuf pa(sizeof(double) * d * m * n, st), pb(sizeof(double) * d * n * l, st);
   DevBuf mua(sizeof(double) * (m + 1), st), mub(sizeof(double) * (l + 1), st);
@@ -274,6 +277,7 @@ void rgemm_ozaki_dev(int k, int64_t m, int64_t n, int64_t l, View A, View B, Vie
     acc_dispatch(k, C, m, l, P.d(), l, st);
   }
   T->renorm_planes(m, l, C, st);
+  return false;
 }
 
 // cgemm_3m / cgemm_4m over the Ozaki real kernel (cmatrix.py:145-169), with
@@ -285,10 +289,31 @@ void cgemm_ozaki_dev(int k, bool use3m, int64_t m, int64_t n, int64_t l, View A,
   View Ar{A.re, nullptr, A.ld, A.ps}, Ai{A.im, nullptr, A.ld, A.ps};
   View Br{B.re, nullptr, B.ld, B.ps}, Bi{B.im, nullptr, B.ld, B.ps};
   size_t ml = sizeof(double) * k * m * l;
-  DevBuf t1(ml, st), t2(ml, st), t3(ml, st), t4(use3m ? 0 : ml, st);
-  DevBuf pre(ml, st), pim(ml, st);
-  View T1 = mk(m, l, t1), T2 = mk(m, l, t2), T3 = mk(m, l, t3), PR = mk(m, l, pre),
-       PI = mk(m, l, pim);
+  DevBuf t1(ml, st), t2(ml, st), t3(use3m ? 0 : ml, st);
+  View T1 = mk(m, l, t1), T2 = mk(m, l, t2), T3 = mk(m, l, t3);
+  View Cr{C.re, nullptr, C.ld, C.ps}, Ci{C.im, nullptr, C.ld, C.ps};
+  // the last real product carries the composition + LU subtraction in its
+  // epilogue on the tensor-core path (OzCombine); otherwise the reference's
+  // mat_add sequence runs as separate passes
+  OzCombine cb{use3m ? 3 : 4, epi, T1, T2, T3, C};
+  auto finish = [&](View Tl) {  // Tl: the last product (T3 for 3M, ri for 4M)
+    DevBuf pre(ml, st), pim(ml, st);
+    View PR = mk(m, l, pre), PI = mk(m, l, pim);
+    T->mat_add(m, l, T1, T2, PR, -1.0, st);
+    if (use3m) {
+      T->mat_add(m, l, Tl, T1, Tl, -1.0, st);
+      T->mat_add(m, l, Tl, T2, PI, -1.0, st);
+    } else {
+      T->mat_add(m, l, T3, Tl, PI, 1.0, st);
+    }
+    if (epi == 1) {
+      T->mat_add(m, l, Cr, PR, Cr, -1.0, st);
+      T->mat_add(m, l, Ci, PI, Ci, -1.0, st);
+    } else {
+      copy_view(k, Cr, PR, m, l, st);
+      copy_view(k, Ci, PI, m, l, st);
+    }
+  };
   if (use3m) {
     DevBuf sa(sizeof(double) * k * m * n, st), sb(sizeof(double) * k * n * l, st);
     View SA = mk(m, n, sa), SB = mk(n, l, sb);
@@ -296,26 +321,16 @@ void cgemm_ozaki_dev(int k, bool use3m, int64_t m, int64_t n, int64_t l, View A,
     rgemm_ozaki_dev(k, m, n, l, Ai, Bi, T2, d, width, st);
     T->mat_add(m, n, Ar, Ai, SA, 1.0, st);
     T->mat_add(n, l, Br, Bi, SB, 1.0, st);
-    rgemm_ozaki_dev(k, m, n, l, SA, SB, T3, d, width, st);
-    T->mat_add(m, l, T1, T2, PR, -1.0, st);
-    T->mat_add(m, l, T3, T1, T3, -1.0, st);
-    T->mat_add(m, l, T3, T2, PI, -1.0, st);
+    DevBuf tl(ml, st);
+    View TL = mk(m, l, tl);
+    if (!rgemm_ozaki_dev(k, m, n, l, SA, SB, TL, d, width, st, &cb)) finish(TL);
   } else {
-    View T4 = mk(m, l, t4);
     rgemm_ozaki_dev(k, m, n, l, Ar, Br, T1, d, width, st);  // rr
     rgemm_ozaki_dev(k, m, n, l, Ai, Bi, T2, d, width, st);  // ii
     rgemm_ozaki_dev(k, m, n, l, Ai, Br, T3, d, width, st);  // ir
-    rgemm_ozaki_dev(k, m, n, l, Ar, Bi, T4, d, width, st);  // ri
-    T->mat_add(m, l, T1, T2, PR, -1.0, st);
-    T->mat_add(m, l, T3, T4, PI, 1.0, st);
-  }
-  View Cr{C.re, nullptr, C.ld, C.ps}, Ci{C.im, nullptr, C.ld, C.ps};
-  if (epi == 1) {
-    T->mat_add(m, l, Cr, PR, Cr, -1.0, st);
-    T->mat_add(m, l, Ci, PI, Ci, -1.0, st);
-  } else {
-    copy_view(k, Cr, PR, m, l, st);
-    copy_view(k, Ci, PI, m, l, st);
+    DevBuf tl(ml, st);
+    View TL = mk(m, l, tl);
+    if (!rgemm_ozaki_dev(k, m, n, l, Ar, Bi, TL, d, width, st, &cb)) finish(TL);  // ri
   }
 }
 

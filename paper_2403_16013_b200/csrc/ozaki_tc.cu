@@ -54,7 +54,7 @@ constexpr int BM = 128;     // MMA M (one TMEM lane per output row)
 constexpr int BKB = 64;     // K bytes per pipeline stage = 2 MMAs of K = 32
 constexpr int NSL = 3;      // digit slices per part
 constexpr int NGRP = 5;     // accumulator groups s = i + j
-constexpr int NEPI = 8;     // epilogue warps (2 per TMEM lane quadrant)
+constexpr int NEPI = 16;    // epilogue warps (4 per TMEM lane quadrant)
 constexpr int NTHR = (NEPI + 2) * 32;  // + producer warp + MMA warp
 constexpr int MAXPAIRS = 160;
 constexpr uint32_t TCOLS = 512;        // two accumulator buffers at columns 0 / 256
@@ -77,6 +77,11 @@ struct Params {
   int64_t m, l, Mp, Lp, Kp;
   int npairs, shift;
   View C;
+  // fused complex composition (OzCombine): 0 = plain C = A B; 3 / 4 = this is
+  // the last real product of a 3M / 4M cgemm, T1 / T2 / T3 hold the earlier
+  // ones; epi = 1 subtracts the complex result from Cc (lu.py:158-161)
+  int mode, epi;
+  View T1, T2, T3, Cc;
   unsigned char pp[MAXPAIRS], pq[MAXPAIRS];
 };
 
@@ -209,6 +214,24 @@ MPC_DI void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
                "r"(r[7])
                : "memory");
 }
+MPC_DI void tmem_ld4(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+MPC_DI void tmem_st4(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+template <int W>
+MPC_DI void tmem_ldw(uint32_t taddr, uint32_t (&r)[8]) {
+  if constexpr (W == 8) tmem_ld8(taddr, r); else tmem_ld4(taddr, r);
+}
+template <int W>
+MPC_DI void tmem_stw(uint32_t taddr, const uint32_t (&r)[8]) {
+  if constexpr (W == 8) tmem_st8(taddr, r); else tmem_st4(taddr, r);
+}
 MPC_DI void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 MPC_DI void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
@@ -228,15 +251,17 @@ MPC_DI void acc_insert(Exp<KL>& c, double q) {
   for (int i = 0; i < KL; i++) c.c[i] = h[i];
 }
 
-// Warp roles: warps 0..7 epilogue (warp w drains TMEM lane quadrant w % 4,
-// column half w / 4), warp 8 producer (one lane issues the bulk copies),
-// warp 9 MMA issuer (one lane).  Pipelines: smem ring full/empty (bulk copy
+// Warp roles: warps 0..15 epilogue (warp w drains TMEM lane quadrant w % 4,
+// column group w / 4), warp 16 producer (one lane issues the bulk copies),
+// warp 17 MMA issuer (one lane).  Pipelines: smem ring full/empty (bulk copy
 // -> MMA -> tcgen05.commit), TMEM double buffer full/empty (MMA -> epilogue).
 template <int KL, int CN>
 __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant__ Params P) {
   using T = Tile<KL>;
-  constexpr int BN = T::BN, S = T::STAGES, HALF = BN / 2;
-  static_assert(HALF % 8 == 0, "column half must be a multiple of the x8 TMEM load");
+  constexpr int BN = T::BN, S = T::STAGES;
+  constexpr int NCG = NEPI / 4, CPT = BN / NCG;  // column groups, columns per thread
+  constexpr int CW = CPT % 8 == 0 ? 8 : 4;       // TMEM load width (x8 or x4)
+  static_assert(CPT % CW == 0, "columns per thread must be a multiple of the TMEM load");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[S], empty[S], accf[2], acce[2];
   __shared__ uint32_t tmem_slot;
@@ -361,12 +386,12 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
     }
   } else {
     // ---------------- epilogue: J = sum_s 2^(b(4-s)) G_s, P = J 2^ea 2^eb, acc_plane
-    const int quad = warp & 3, half = warp >> 2;
+    const int quad = warp & 3, cgrp = warp >> 2;
     const int64_t grow = row0 + quad * 32 + lane;
-    const int cbase = half * HALF;
-    Exp<KL> acc[HALF];
+    const int cbase = cgrp * CPT;
+    Exp<KL> acc[CPT];
 #pragma unroll
-    for (int j = 0; j < HALF; j++) acc[j] = exp_zero<KL>();
+    for (int j = 0; j < CPT; j++) acc[j] = exp_zero<KL>();
     const int b = P.shift;
     // zero this thread's accumulator columns of both buffers (the MMAs always
     // accumulate), then hand the buffers to the MMA warp
@@ -376,7 +401,7 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
 #pragma unroll
       for (int g = 0; g < NGRP; g++)
 #pragma unroll
-        for (int cc = 0; cc < HALF / 8; cc++) tmem_st8(tq + (uint32_t)(bb * 256 + g * BN + cc * 8), z);
+        for (int cc = 0; cc < CPT / CW; cc++) tmem_stw<CW>(tq + (uint32_t)(bb * 256 + g * BN + cc * CW), z);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&acce[bb]);
@@ -389,42 +414,75 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
       const double sav = grow < P.m ? P.scale_a[(int64_t)P.pp[t] * P.m + grow] : 0.0;
       const double* sbp = P.scale_b + (int64_t)P.pq[t] * P.l;
 #pragma unroll
-      for (int cc = 0; cc < HALF / 8; cc++) {
+      for (int cc = 0; cc < CPT / CW; cc++) {
         uint32_t r[NGRP][8];
 #pragma unroll
-        for (int g = 0; g < NGRP; g++) tmem_ld8(trow + (uint32_t)(g * BN + cc * 8), r[g]);
+        for (int g = 0; g < NGRP; g++) tmem_ldw<CW>(trow + (uint32_t)(g * BN + cc * CW), r[g]);
         tmem_wait_ld();
 #pragma unroll
-        for (int g = 0; g < NGRP; g++) tmem_st8(trow + (uint32_t)(g * BN + cc * 8), z);
-        if (cc == HALF / 8 - 1) {
+        for (int g = 0; g < NGRP; g++) tmem_stw<CW>(trow + (uint32_t)(g * BN + cc * CW), z);
+        if (cc == CPT / CW - 1) {
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&acce[buf]);  // drained and re-zeroed for pair t + 2
         }
 #pragma unroll
-        for (int jj = 0; jj < 8; jj++) {
+        for (int jj = 0; jj < CW; jj++) {
           long long J = (long long)(int)r[0][jj];
 #pragma unroll
           for (int g = 1; g < NGRP; g++) J = J * (1ll << b) + (long long)(int)r[g][jj];
-          const int64_t gc = col0 + cbase + cc * 8 + jj;
+          const int64_t gc = col0 + cbase + cc * CW + jj;
           const double sbv = gc < P.l ? sbp[gc] : 0.0;
           const double v = __dmul_rn(__dmul_rn(__ll2double_rn(J), sav), sbv);
-          acc_insert<KL>(acc[cc * 8 + jj], v);
+          acc_insert<KL>(acc[cc * CW + jj], v);
         }
       }
     }
-    // renorm_planes (_kernels.py:485-499) and store
-    if (grow < P.m) {
+    // renorm_planes (_kernels.py:485-499) into a shared-memory tile (the
+    // operand ring is idle now: every stage has been consumed), then a
+    // coalesced pass over the tile stores C -- or applies the fused complex
+    // composition / LU subtraction (OzCombine) elementwise.
+    constexpr int OS = BN + 1;  // padded row stride (doubles)
+    static_assert(KL * BM * OS * 8 <= T::SMEM, "output tile must fit the ring");
+    double* otile = reinterpret_cast<double*>(smem);
+    const int lrow = quad * 32 + lane;
 #pragma unroll
-      for (int j = 0; j < HALF; j++) {
-        const int64_t gc = col0 + cbase + j;
-        if (gc < P.l) {
-          double bufv[KL];
+    for (int j = 0; j < CPT; j++) {
+      double bufv[KL];
 #pragma unroll
-          for (int c = 0; c < KL; c++) bufv[c] = acc[j].c[c];
-          Exp<KL> o = renorm<KL, KL>(bufv, KL);
-          stexp_<KL>(P.C.re + grow * P.C.ld + gc, P.C.ps, o);
+      for (int c = 0; c < KL; c++) bufv[c] = acc[j].c[c];
+      Exp<KL> o = renorm<KL, KL>(bufv, KL);
+#pragma unroll
+      for (int c = 0; c < KL; c++) otile[(c * BM + lrow) * OS + cbase + j] = o.c[c];
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(NEPI * 32) : "memory");
+    for (int e = tid; e < BM * BN; e += NEPI * 32) {
+      const int row = e / BN, col = e % BN;
+      const int64_t gr = row0 + row, gc = col0 + col;
+      if (gr >= P.m || gc >= P.l) continue;
+      Exp<KL> o;
+#pragma unroll
+      for (int c = 0; c < KL; c++) o.c[c] = otile[(c * BM + row) * OS + col];
+      if (P.mode == 0) {
+        stexp_<KL>(P.C.re + gr * P.C.ld + gc, P.C.ps, o);
+      } else {
+        // cmatrix.py:153 / 166-168 and lu.py:158-161, elementwise in the
+        // reference's order (mat_add_k with sign -1 == exp_sub)
+        const Exp<KL> t1 = ldexp_<KL>(P.T1.re + gr * P.T1.ld + gc, P.T1.ps);
+        const Exp<KL> t2 = ldexp_<KL>(P.T2.re + gr * P.T2.ld + gc, P.T2.ps);
+        Exp<KL> re = exp_sub(t1, t2), im;
+        if (P.mode == 3) {
+          im = exp_sub(exp_sub(o, t1), t2);  // (T3 - T1) - T2, o = T3
+        } else {
+          im = exp_add(ldexp_<KL>(P.T3.re + gr * P.T3.ld + gc, P.T3.ps), o);  // ir + ri
         }
+        const int64_t off = gr * P.Cc.ld + gc;
+        if (P.epi) {
+          re = exp_sub(ldexp_<KL>(P.Cc.re + off, P.Cc.ps), re);
+          im = exp_sub(ldexp_<KL>(P.Cc.im + off, P.Cc.ps), im);
+        }
+        stexp_<KL>(P.Cc.re + off, P.Cc.ps, re);
+        stexp_<KL>(P.Cc.im + off, P.Cc.ps, im);
       }
     }
   }
@@ -439,89 +497,108 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
 }
 
 // Fused ozaki_split (ozaki.py:79-108) of one operand, straight to digit
-// slices: one CTA per grid line (a row of the left operand, a column of the
-// right one), its k-limb residual held in shared memory for all d steps:
-//   mu = max |r0| (block reduction), (f, ex) = frexp(mu), S = 2^ex 2^(53-width),
+// slices.  A CTA owns NL grid lines (rows of the left operand, columns of the
+// right one); their k-limb residuals stay in shared memory for all d steps:
+//   mu = max |r0| per line, (f, ex) = frexp(mu), S = 2^ex 2^(53-width),
 //   part = (r0 + S) - S, r0 -= part, renorm the limbs (renorm_planes),
-//   scale = 2^(ex - width), I = part / scale -> NSL digits (tiled layout).
-// The element sequence of each step is the reference's, elementwise, so the
-// parts and grids are bit-identical to ozaki_split's.
-// src element (r, t): trans == 0 -> src[r*ld + t] (left: rows of A),
-//                     trans == 1 -> src[t*ld + r] (right: columns of B).
+//   scale = 2^(ex - width), I = part / scale -> NSL balanced digits.
+// Each element sees exactly the reference's operation sequence, so parts and
+// grids are bit-identical to ozaki_split's.
+// src element (r, t): trans == 0 -> src[r*ld + t] (left), src[t*ld + r]
+// (right).  Loads are coalesced along the contiguous index; the compute phase
+// gives thread (line tl = tid % NL, tt = tid / NL) the 16-deep K groups
+// tt, tt + 256/NL, ... of its line (one int4 store per digit slice); lines are
+// padded to an odd stride in shared memory (conflict-free).
 template <int KL>
 __global__ void __launch_bounds__(256) split_lines_kernel(const double* src, int64_t ld, int64_t ps,
-                                                          int trans, int64_t R, int64_t n, int d,
-                                                          int width, int shift, int8_t* out,
-                                                          int64_t Rp, int64_t Kp, int TR,
-                                                          int stackB, double* scale) {
-  extern __shared__ double res[];  // [KL][n]
-  __shared__ double red[8];
-  const int64_t r = blockIdx.x;
+                                                          int trans, int64_t R, int64_t n, int NL,
+                                                          int d, int width, int shift,
+                                                          int8_t* out, int64_t Rp, int64_t Kp,
+                                                          int TR, int stackB, double* scale) {
+  extern __shared__ double res[];  // [KL][NL][n | 1]
+  __shared__ double red[256];
   const int tid = threadIdx.x;
-  for (int64_t t = tid; t < n; t += blockDim.x)
+  const int64_t r0 = (int64_t)blockIdx.x * NL;
+  const int64_t ls = n | 1;  // odd line stride (doubles)
+  const int64_t cs = ls * NL;
+  for (int64_t idx = tid; idx < (int64_t)NL * n; idx += 256) {
+    const int64_t line = trans ? idx % NL : idx / n, t = trans ? idx / NL : idx % n;
+    const int64_t r = r0 + line;
 #pragma unroll
     for (int c = 0; c < KL; c++)
-      res[c * n + t] = trans ? src[c * ps + t * ld + r] : src[c * ps + r * ld + t];
+      res[c * cs + line * ls + t] =
+          r < R ? (trans ? src[c * ps + t * ld + r] : src[c * ps + r * ld + t]) : 0.0;
+  }
   __syncthreads();
+  const int TPL = 256 / NL;  // threads per line
+  const int tl = tid % NL, tt = tid / NL;
+  const int64_t r = r0 + tl;
   const int64_t kch = Kp / 16, slice = Rp * Kp;
+  const int64_t sstride = stackB ? (int64_t)TR * 16 : slice;
+  const int64_t gstride = stackB ? (int64_t)NSL * TR * 16 : (int64_t)TR * 16;
   const long long mask = (1ll << shift) - 1, half = 1ll << (shift - 1);
   const double shiftS = ldexp(1.0, 53 - width);
+  const int64_t ng = (n + 15) / 16;
+  double* line0 = res + tl * ls;
   for (int p = 0; p < d; p++) {
     double m = 0.0;
-    for (int64_t t = tid; t < n; t += blockDim.x) m = fmax(m, fabs(res[t]));
+    for (int64_t g = tt; g < ng; g += TPL)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((tid & 31) == 0) red[tid >> 5] = m;
+      for (int i = 0; i < 16; i++)
+        if (g * 16 + i < n) m = fmax(m, fabs(line0[g * 16 + i]));
+    red[tid] = m;
     __syncthreads();
-    m = red[0];
-#pragma unroll
-    for (int w = 1; w < 8; w++) m = fmax(m, red[w]);
+    // max over the TPL threads of each line (they sit at stride NL)
+    if (tt == 0) {
+      for (int w = 1; w < TPL; w++) m = fmax(m, red[tl + w * NL]);
+      red[tl] = m;  // (slots >= NL are only read above: no race)
+    }
+    __syncthreads();
+    m = red[tl];
     __syncthreads();  // red reused next step
     int ex = 0;
     frexp(m, &ex);
     const double w = ldexp(1.0, ex);
     const double S = __dmul_rn(w, shiftS);
     const int es = ex - width;  // scale = ldexp(w, -width) = 2^es
-    if (tid == 0) scale[(int64_t)p * R + r] = ldexp(w, -width);
-    // left (stackB = 0): [p][s][R/TR][kch][TR][16]; right (stackB = 1):
-    // [p][R/TR][kch][s][TR][16] (the three slices of a K chunk stacked)
-    const int64_t sstride = stackB ? (int64_t)TR * 16 : slice;
-    const int64_t gstride = stackB ? (int64_t)NSL * TR * 16 : (int64_t)TR * 16;
-    int8_t* o = out + (int64_t)p * NSL * slice + ((r / TR) * kch) * gstride + (r % TR) * 16;
-    for (int64_t g = tid; g < (n + 15) / 16; g += blockDim.x) {
-      union {
-        int8_t b[16];
-        int4 v;
-      } d0, d1, d2;
+    if (tt == 0 && r < R) scale[(int64_t)p * R + r] = ldexp(w, -width);
+    if (r < R) {
+      int8_t* o = out + (int64_t)p * NSL * slice + ((r / TR) * kch) * gstride + (r % TR) * 16;
+      for (int64_t g = tt; g < ng; g += TPL) {
+        union {
+          int8_t b[16];
+          int4 v;
+        } d0, d1, d2;
 #pragma unroll
-      for (int tt = 0; tt < 16; tt++) {
-        const int64_t t = g * 16 + tt;
-        long long I = 0;
-        if (t < n) {
-          const double r0 = res[t];
-          const double pt = __dsub_rn(__dadd_rn(r0, S), S);
-          double buf[KL];
-          buf[0] = __dsub_rn(r0, pt);
+        for (int i = 0; i < 16; i++) {
+          const int64_t t = g * 16 + i;
+          long long I = 0;
+          if (t < n) {
+            const double x0 = line0[t];
+            const double pt = __dsub_rn(__dadd_rn(x0, S), S);
+            double buf[KL];
+            buf[0] = __dsub_rn(x0, pt);
 #pragma unroll
-          for (int c = 1; c < KL; c++) buf[c] = res[c * n + t];
-          Exp<KL> e = renorm<KL, KL>(buf, KL);
+            for (int c = 1; c < KL; c++) buf[c] = line0[c * cs + t];
+            Exp<KL> e = renorm<KL, KL>(buf, KL);
 #pragma unroll
-          for (int c = 0; c < KL; c++) res[c * n + t] = e.c[c];
-          I = __double2ll_rn(ldexp(pt, -es));  // exact: pt is a multiple of 2^es
+            for (int c = 0; c < KL; c++) line0[c * cs + t] = e.c[c];
+            I = __double2ll_rn(ldexp(pt, -es));  // exact: pt is a multiple of 2^es
+          }
+          // balanced signed digits: I = a0 2^(2b) + a1 2^b + a2, a1, a2 in
+          // [-2^(b-1), 2^(b-1)), |a0| <= 2^(w-2b) + 1 -- all s8
+          const long long a2 = ((I + half) & mask) - half;
+          const long long I1 = (I - a2) >> shift;
+          const long long a1 = ((I1 + half) & mask) - half;
+          d0.b[i] = (int8_t)((I1 - a1) >> shift);
+          d1.b[i] = (int8_t)a1;
+          d2.b[i] = (int8_t)a2;
         }
-        // balanced signed digits: I = a0 2^(2b) + a1 2^b + a2, a1, a2 in
-        // [-2^(b-1), 2^(b-1)), |a0| <= 2^(w-2b) + 1 -- all s8
-        const long long a2 = ((I + half) & mask) - half;
-        const long long I1 = (I - a2) >> shift;
-        const long long a1 = ((I1 + half) & mask) - half;
-        d0.b[tt] = (int8_t)((I1 - a1) >> shift);
-        d1.b[tt] = (int8_t)a1;
-        d2.b[tt] = (int8_t)a2;
+        int8_t* og = o + g * gstride;
+        *reinterpret_cast<int4*>(og) = d0.v;
+        *reinterpret_cast<int4*>(og + sstride) = d1.v;
+        *reinterpret_cast<int4*>(og + 2 * sstride) = d2.v;
       }
-      int8_t* og = o + g * gstride;
-      *reinterpret_cast<int4*>(og) = d0.v;
-      *reinterpret_cast<int4*>(og + sstride) = d1.v;
-      *reinterpret_cast<int4*>(og + 2 * sstride) = d2.v;
     }
     __syncthreads();
   }
@@ -635,7 +712,8 @@ bool ozaki_tc_enabled() {
 }
 
 bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View C, int d,
-                    const std::vector<std::pair<int, int>>& pairs, int width, cudaStream_t st) {
+                    const std::vector<std::pair<int, int>>& pairs, int width, cudaStream_t st,
+                    const OzCombine* cb) {
   using namespace otc;
   if (k < 2 || k > 4 || m <= 0 || l <= 0 || n <= 0) return false;
   if ((int)pairs.size() > MAXPAIRS || d > 255) return false;
@@ -651,8 +729,7 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
     return false;
   }
   if (gmax * (double)n >= 2147483648.0) return false;
-  const size_t line_smem = sizeof(double) * (size_t)k * (size_t)n;
-  if (line_smem > 200 * 1024) return false;
+  if (sizeof(double) * (size_t)k * (size_t)(n | 1) > 200 * 1024) return false;
   const int BN = k == 2 ? Tile<2>::BN : Tile<3>::BN;
   const int64_t LT = (int64_t)BN * cluster_n();  // column tiles come in whole clusters
   const int64_t Mp = (m + BM - 1) / BM * BM, Lp = (l + LT - 1) / LT * LT,
@@ -681,8 +758,11 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
                            200 * 1024);
       attr = true;
     }
-    split_lines_kernel<KL><<<(unsigned)R, 256, line_smem, st>>>(src, ld, ps, trans, R, n, d, width,
-                                                                shift, out, Rp, Kp, TR, stackB, sc);
+    int NL = 16;  // lines per CTA: as many as fit 200 KB of residual
+    while (NL > 1 && (size_t)NL * (size_t)(n | 1) * KL * 8 > 200 * 1024) NL /= 2;
+    const size_t smem = (size_t)NL * (size_t)(n | 1) * KL * 8;
+    split_lines_kernel<KL><<<(unsigned)((R + NL - 1) / NL), 256, smem, st>>>(
+        src, ld, ps, trans, R, n, NL, d, width, shift, out, Rp, Kp, TR, stackB, sc);
   };
   switch (k) {
     case 2:
@@ -714,6 +794,14 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
   P.npairs = (int)pairs.size();
   P.shift = shift;
   P.C = C;
+  if (cb) {
+    P.mode = cb->mode;
+    P.epi = cb->epi;
+    P.T1 = cb->T1;
+    P.T2 = cb->T2;
+    P.T3 = cb->T3;
+    P.Cc = cb->Cc;
+  }
   for (size_t i = 0; i < pairs.size(); i++) {
     P.pp[i] = (unsigned char)pairs[i].first;
     P.pq[i] = (unsigned char)pairs[i].second;
