@@ -255,7 +255,7 @@ MPC_DI void acc_insert(Exp<KL>& c, double q) {
 // column group w / 4), warp 16 producer (one lane issues the bulk copies),
 // warp 17 MMA issuer (one lane).  Pipelines: smem ring full/empty (bulk copy
 // -> MMA -> tcgen05.commit), TMEM double buffer full/empty (MMA -> epilogue).
-template <int KL, int CN>
+template <int KL, int CN, int SB>
 __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant__ Params P) {
   using T = Tile<KL>;
   constexpr int BN = T::BN, S = T::STAGES;
@@ -392,7 +392,6 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
     Exp<KL> acc[CPT];
 #pragma unroll
     for (int j = 0; j < CPT; j++) acc[j] = exp_zero<KL>();
-    const int b = P.shift;
     // zero this thread's accumulator columns of both buffers (the MMAs always
     // accumulate), then hand the buffers to the MMA warp
     const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)cbase;
@@ -428,11 +427,16 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
         }
 #pragma unroll
         for (int jj = 0; jj < CW; jj++) {
-          long long J = (long long)(int)r[0][jj];
-#pragma unroll
-          for (int g = 1; g < NGRP; g++) J = J * (1ll << b) + (long long)(int)r[g][jj];
+          // J = sum_s 2^(SB (4 - s)) G_s as int32 x constant -> int64
+          // multiply-adds (exact: |J| <= 2^53)
+          long long J = (long long)(int)r[4][jj];
+          J += (long long)(int)r[3][jj] * (1ll << SB);
+          J += (long long)(int)r[2][jj] * (1ll << (2 * SB));
+          J += (long long)(int)r[1][jj] * (1ll << (3 * SB));
+          J += (long long)(int)r[0][jj] * (1ll << (4 * SB));
           const int64_t gc = col0 + cbase + cc * CW + jj;
           const double sbv = gc < P.l ? sbp[gc] : 0.0;
+          // P = J 2^ea 2^eb: exact binary64 (the grids are powers of two)
           const double v = __dmul_rn(__dmul_rn(__ll2double_rn(J), sav), sbv);
           acc_insert<KL>(acc[cc * CW + jj], v);
         }
@@ -609,11 +613,11 @@ unsigned grid_for(int64_t total) {
   return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
 }
 
-template <int KL, int CN>
+template <int KL, int CN, int SB>
 void launch_cn(const Params& P, cudaStream_t st, double ops) {
   using T = Tile<KL>;
   static bool attr = false;
-  auto kern = ozaki_tc_kernel<KL, CN>;
+  auto kern = ozaki_tc_kernel<KL, CN, SB>;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
     attr = true;
@@ -640,8 +644,8 @@ void launch_cn(const Params& P, cudaStream_t st, double ops) {
 inline int cluster_n() {
   static int cn = [] {
     const char* e = getenv("MPC_OZAKI_CLUSTER");
-    int v = e ? atoi(e) : 4;
-    return (v == 1 || v == 2 || v == 4) ? v : 4;
+    int v = e ? atoi(e) : 1;  // multicast measured no faster at LU shapes (K = 512)
+    return v == 2 ? 2 : 1;
   }();
   return cn;
 }
@@ -649,9 +653,12 @@ inline int cluster_n() {
 template <int KL>
 void launch(const Params& P, cudaStream_t st, double ops) {
   switch (cluster_n()) {
-    case 1: launch_cn<KL, 1>(P, st, ops); break;
-    case 2: launch_cn<KL, 2>(P, st, ops); break;
-    default: launch_cn<KL, 4>(P, st, ops); break;
+    case 2:
+      if (P.shift == 7) launch_cn<KL, 2, 7>(P, st, ops); else launch_cn<KL, 2, 8>(P, st, ops);
+      break;
+    default:
+      if (P.shift == 7) launch_cn<KL, 1, 7>(P, st, ops); else launch_cn<KL, 1, 8>(P, st, ops);
+      break;
   }
 }
 
