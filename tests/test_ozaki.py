@@ -102,3 +102,81 @@ def test_gpu_ozaki_vs_oracle_sizes(orc):
         A = mp.random_matrix(m, n, k, rng)
         B = mp.random_matrix(n, l, k, rng)
         assert beq(mp.rgemm_ozaki(A, B, d).data, ozr.rgemm(A.data, B.data, d)), (m, n, l, k)
+
+
+def _both_paths(monkeypatch, fn):
+    """fn() on the binary64 seam (cuBLAS DGEMM) and on the INT8 tensor-core path."""
+    monkeypatch.setenv("MPC_OZAKI_GEMM", "dgemm")
+    a = fn()
+    monkeypatch.setenv("MPC_OZAKI_GEMM", "tc")
+    b = fn()
+    return a, b
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_gpu_ozaki_tensor_core_equals_seam(monkeypatch, k):
+    """The tcgen05 INT8 path (digit slices, int32 TMEM groups, fused acc_plane /
+    renorm / complex composition) is bit-identical to the exact binary64 seam:
+    ragged row / column tiles, inner sizes off the 64-deep stage, several
+    column tiles, both digit bases (width <= 20: base 2^7; 21..22: base 2^8)."""
+    import paper_2403_16013_b200 as mp
+
+    rng = np.random.default_rng(100 + k)
+    d = {2: 6, 3: 8, 4: 12}[k]
+    for (m, n, l) in [(1, 1, 1), (130, 70, 33), (257, 100, 97), (129, 1000, 130), (64, 64, 200)]:
+        A = mp.random_matrix(m, n, k, rng)
+        B = mp.random_matrix(n, l, k, rng)
+        for sb in (None, 12, min(21, mp.split_exactness_bound(n))):
+            x, y = _both_paths(monkeypatch, lambda: mp.rgemm_ozaki(A, B, d, split_bits=sb).data)
+            assert beq(x, y), (m, n, l, k, sb)
+    P = [mp.PlanarComplexMatrix(mp.random_matrix(90, 77, k, rng), mp.random_matrix(90, 77, k, rng)),
+         mp.PlanarComplexMatrix(mp.random_matrix(77, 110, k, rng), mp.random_matrix(77, 110, k, rng))]
+    for meth in ("3m", "4m"):
+        kc = mp.KernelChoice(method=meth, real_kernel="ozaki")
+        x, y = _both_paths(monkeypatch, lambda: mp.cgemm(P[0], P[1], kc))
+        assert beq(x.re_plane.data, y.re_plane.data) and beq(x.im_plane.data, y.im_plane.data), meth
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("meth", ["3m", "4m"])
+def test_gpu_ozaki_lu_tensor_core_equals_seam(monkeypatch, meth):
+    """lu_blocked with real_kernel="ozaki": the lookahead schedule with the fused
+    LU subtraction on the tensor cores gives the seam's pivots and factors."""
+    import paper_2403_16013_b200 as mp
+    from paper_2403_16013_b200 import problems
+
+    re, im = problems.lu_matrix(150, 2, 5)
+    A = mp.PlanarComplexMatrix(mp.RealMatrix(re), mp.RealMatrix(im))
+    kc = mp.KernelChoice(method=meth, real_kernel="ozaki")
+    x, y = _both_paths(monkeypatch, lambda: mp.lu_blocked(A, 32, kc=kc))
+    assert np.array_equal(x.pivots, y.pivots)
+    assert beq(x.packed.re_plane.data, y.packed.re_plane.data)
+    assert beq(x.packed.im_plane.data, y.packed.im_plane.data)
+
+
+@pytest.mark.gpu
+def test_gpu_ozaki_cluster_multicast():
+    """MPC_OZAKI_CLUSTER=2 (A tiles multicast to a 2-CTA cluster) gives the same bits
+    (the cluster size is read once per process, hence the subprocess)."""
+    import subprocess
+    import sys
+
+    code = ("import os,sys,numpy as np; sys.path.insert(0, %r);"
+            "import paper_2403_16013_b200 as mp;"
+            "r=np.random.default_rng(7); A=mp.random_matrix(300,200,2,r); B=mp.random_matrix(200,250,2,r);"
+            "os.environ['MPC_OZAKI_GEMM']='dgemm'; x=mp.rgemm_ozaki(A,B,6).data;"
+            "os.environ['MPC_OZAKI_GEMM']='tc'; y=mp.rgemm_ozaki(A,B,6).data;"
+            "print('EQ', x.tobytes()==y.tobytes())") % os.path.dirname(os.path.dirname(__file__))
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "MPC_OZAKI_CLUSTER": "2"},
+                         capture_output=True, text=True, timeout=300)
+    assert "EQ True" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+def test_gpu_int8_peak_measured():
+    """The INT8 tensor-core roofline denominator is measured, not assumed."""
+    from paper_2403_16013_b200 import device
+
+    p = device.int8_peak(50000)
+    assert 1e15 < p < 1e16
