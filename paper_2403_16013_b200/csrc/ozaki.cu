@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -499,7 +501,19 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
     cudaEvent_t ev_narrow, ev_panel;
     cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+    // MPC_TRACE=1: per-step timeline on stderr (as mpc_getrf)
+    static const bool trace = getenv("MPC_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t s) {
+      if (!trace) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      tev.push_back(e);
+    };
+    mark(st);
     T->panel_rec(use3m, A, n, 0, std::min(K, n), dp, w.ws, st);
+    mark(st);
     for (int64_t jb = 0; jb < n; jb += K) {
       int64_t kw = std::min(K, n - jb);
       int64_t end = jb + kw;
@@ -508,11 +522,33 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
       int64_t kw2 = std::min(K, n - end);
       update_cols(jb, kw, end, end + kw2, st);
       cudaEventRecord(ev_narrow, st);
+      mark(st);
       cudaStreamWaitEvent(sp, ev_narrow, 0);
       T->panel_rec(use3m, A, n, end, kw2, dp, w.ws, sp);
       cudaEventRecord(ev_panel, sp);
+      mark(sp);
       update_cols(jb, kw, end + kw2, n, st);
+      mark(st);
       cudaStreamWaitEvent(st, ev_panel, 0);
+      mark(st);
+    }
+    if (trace) {
+      cudaStreamSynchronize(st);
+      float t;
+      cudaEventElapsedTime(&t, tev[0], tev[1]);
+      fprintf(stderr, "MPC_TRACE ozaki n=%lld K=%lld first-panel %.3f ms\n", (long long)n,
+              (long long)K, t);
+      for (size_t i = 1; i + 4 < tev.size(); i += 4) {
+        float tn, tp, tr, tj;
+        cudaEventElapsedTime(&tn, tev[i], tev[i + 1]);
+        cudaEventElapsedTime(&tp, tev[i + 1], tev[i + 2]);
+        cudaEventElapsedTime(&tr, tev[i + 1], tev[i + 3]);
+        cudaEventElapsedTime(&tj, tev[i], tev[i + 4]);
+        fprintf(stderr,
+                "MPC_TRACE step %zu: narrow %.3f  panel(side) %.3f  rest %.3f  step %.3f ms\n",
+                (i - 1) / 4, tn, tp, tr, tj);
+      }
+      for (auto e : tev) cudaEventDestroy(e);
     }
     cudaEventDestroy(ev_narrow);
     cudaEventDestroy(ev_panel);
