@@ -410,8 +410,13 @@ def run_gemm(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    ozaki = args.real_kernel == "ozaki"
+
     def gemm():
-        device.cgemm(*T, cr, ci, method=args.method)
+        if ozaki:
+            device.cgemm_ozaki(*T, cr, ci, method=args.method)
+        else:
+            device.cgemm(*T, cr, ci, method=args.method)
 
     for _ in range(args.warmup):
         gemm()
@@ -431,18 +436,32 @@ def run_gemm(args):
     launches = _lib.launch_count() - l0
     ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     ms_step = statistics.mean(ms)
-    ops = n ** 3 * (93 if args.method == "3m" else 124) * (1 if k == 2 else 0)
-    ach = ops / (ms_step * 1e-3) / 1e12
+    if ozaki:
+        _lib.prof_enable(True, classes=["gemm"])
+        gemm()
+        torch.cuda.synchronize()
+        g_ms, g_ops, _ = _lib.prof_summary()["gemm"]
+        _lib.prof_enable(False)
+        pk = device.int8_peak()
+        ach = g_ops / (g_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk / 1e12, "frac": ach * 1e12 / pk,
+                "unit": "TOP/s (INT8 tensor-core ops, ozaki_tc_kernel launches only)",
+                "traffic": None}
+    else:
+        opm = {2: (93, 124), 3: (585, 780), 4: (975, 1300)}[k][0 if args.method == "3m" else 1]
+        ach = n ** 3 * opm / (ms_step * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": peak / 1e12, "frac": ach * 1e12 / peak,
+                "unit": "TFLOP/s (FP64 instr/s, op model v1)", "traffic": None}
     from paper_2403_16013_b200.digest import digest
 
     out = {"metric": "complex-DD GEMM GFLOPS (8n³ conv.) & % FP64 peak", "value":
            8.0 * n ** 3 / (ms_step * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (DD)",
-           "data": "synthetic", "config": {"workload": f"cfg1: complex DD GEMM n={n} {args.method}",
+           "data": "synthetic", "config": {"workload": f"cfg1: complex {dict([(2, 'DD'), (3, 'TD'), (4, 'QD')])[k]} GEMM n={n} {args.method}"
+                                            + (" real_kernel=ozaki" if ozaki else ""),
                                             "l2": "512 MiB buffer written between timed GEMMs"},
-           "roofline": {"bound": "fp64", "achieved": ach, "peak": peak / 1e12, "frac":
-                        ach * 1e12 / peak, "unit": "TFLOP/s (FP64 instr/s)", "traffic": None},
+           "roofline": roof, "real_kernel": args.real_kernel,
            "gemm_variant": os.environ.get("MPC_GEMM_VARIANT", "0"),
            "digest": digest(cr.cpu().numpy(), ci.cpu().numpy()), "gpu_launches": launches}
     print(json.dumps(out), flush=True)
