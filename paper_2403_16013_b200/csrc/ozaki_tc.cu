@@ -267,7 +267,24 @@ __global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant
   __shared__ uint32_t tmem_slot;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t ct = blockIdx.x, rt = blockIdx.y;  // column tile, row tile
+  // column tile / row tile.  Without clusters: grouped raster -- 8 row tiles
+  // sweep the column tiles together, so each B slice tile is fetched from
+  // DRAM once per group instead of once per row tile (the A tiles of the
+  // group stay L2-resident).  With clusters: the cluster shares a row tile.
+  int64_t ct, rt;
+  if constexpr (CN == 1) {
+    constexpr int64_t G = 8;
+    const int64_t tiles_m = P.Mp / BM, tiles_n = P.Lp / BN;
+    const int64_t bid = blockIdx.x;
+    const int64_t grp = bid / (G * tiles_n), first_m = grp * G;
+    const int64_t gsz = tiles_m - first_m < G ? tiles_m - first_m : G;
+    const int64_t in_grp = bid - grp * G * tiles_n;
+    rt = first_m + in_grp % gsz;
+    ct = in_grp / gsz;
+  } else {
+    ct = blockIdx.x;
+    rt = blockIdx.y;
+  }
   const int64_t col0 = ct * BN, row0 = rt * BM;
 
   if (tid == 0) {
@@ -623,7 +640,8 @@ void launch_cn(const Params& P, cudaStream_t st, double ops) {
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(P.Lp / T::BN), (unsigned)(P.Mp / BM));
+  cfg.gridDim = CN == 1 ? dim3((unsigned)((P.Lp / T::BN) * (P.Mp / BM)))
+                        : dim3((unsigned)(P.Lp / T::BN), (unsigned)(P.Mp / BM));
   cfg.blockDim = dim3(NTHR);
   cfg.dynamicSmemBytes = T::SMEM;
   cfg.stream = st;
