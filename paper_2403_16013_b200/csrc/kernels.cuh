@@ -1037,7 +1037,15 @@ struct Ops {
     trsm(use3m, kb - h, M, L.sub(h, h), X.sub(h, 0), st, status);
   }
 
-  static constexpr int PANEL_BASE = PanelCluster<K>::WMAX;
+  // base-panel width (<= WMAX); MPC_PANEL_BASE overrides for experiments
+  static int panel_base_w() {
+    static int b = [] {
+      const char* e = getenv("MPC_PANEL_BASE");
+      int v = e ? atoi(e) : PanelCluster<K>::WMAX;
+      return (v >= 1 && v <= PanelCluster<K>::WMAX) ? v : PanelCluster<K>::WMAX;
+    }();
+    return b;
+  }
   // base panel: columns [c0, c0+w) over rows [c0, n), swaps within [c0, c0+w)
   // cluster size for the base panel: the largest of 16 / 8 / 4 / 2 that can
   // be co-scheduled (0 = use the per-column launches; MPC_PANEL=launches)
@@ -1114,6 +1122,7 @@ struct Ops {
   // interchange piv[c0..c0+w) has been applied to columns [c0, c0+w)
   static void panel_rec(bool use3m, View A, int64_t n, int64_t c0, int64_t w, int64_t* piv,
                         PanelWs ws, cudaStream_t st) {
+    const int64_t PANEL_BASE = panel_base_w();
     if (w <= PANEL_BASE) {
       panel_base(use3m, A, n, c0, w, piv, ws, st);
       return;
