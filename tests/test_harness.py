@@ -56,8 +56,8 @@ def test_factor_op_model():
     # K = n: a single panel, no TRSM / GEMM: n (n-1)/2 * n-ish panel updates
     ops = hb._factor_ops(4, 4, 2, "3m", True)
     assert ops == (3 * 3 + 2 * 2 + 1 * 1) * 173   # sum_j (rows below j) (columns right of j)
-    # blocked: trailing update contributes M^2 K * 93
-    assert hb._factor_ops(8, 4, 2, "3m", False) > hb._factor_ops(8, 8, 2, "3m", True)
+    # n = 8, K = 4: panels 38 + 14 updates, TRSM 4 * 6, GEMM 4 * 4 * 4 complex MACs
+    assert hb._factor_ops(8, 4, 2, "3m", False) == (38 + 14 + 24) * 173 + 64 * 93
 
 
 def test_cli_usage_errors():
