@@ -100,36 +100,39 @@ MPC_DI Exp<K> exp_abs(const Exp<K>& x) {
   return (x.c[0] < 0.0) ? exp_neg(x) : x;
 }
 
-// sort key for (|v| desc, v desc), offset by one so that 0 can mark padding
-// slots: equal keys <=> identical values, or zeros of either sign (the
-// reference's insertion sort does not order +0 / -0 either).
+// Sort key for (|v| desc, v desc): (absbits << 1) | !sign -- a bijection on
+// non-NaN doubles, so the network sorts the keys alone and the values are
+// rebuilt from them afterwards (one 64-bit max / min pair per comparator).
+// The order equals the reference's except among zeros (+0 now precedes -0,
+// the reference treats them as equal): zeros always form the tail and their
+// order cannot change the VecSum sweep (every TwoSum of two zeros gives the
+// same sum and a +0 error in either order), so renorm's output is
+// bit-identical.  Padding slots (i >= m) get key 0 (= -0): they sink to the
+// end, and a padding key that ties with a real -0 rebuilds the same -0.
 MPC_DI uint64_t sort_key(double v) {
-  uint64_t a = absbits(v);
-  uint64_t pos = (a != 0ull && !(bits(v) >> 63)) ? 1ull : 0ull;
-  return ((a << 1) | pos) + 1ull;
+  const uint64_t b = bits(v);
+  return (b << 1) | ((b >> 63) ^ 1ull);
+}
+MPC_DI double from_key(uint64_t k) {
+  return __longlong_as_double((long long)((k >> 1) | ((~k & 1ull) << 63)));
 }
 
 // _sort_desc, _kernels.py:67-78, on buf[0..m) (m <= M, runtime).  A sorting
 // network (sortnet.h) replaces the insertion sort: the sorted sequence is
 // the same except for the relative order of equal keys, i.e. identical
-// values (no effect) or signed zeros, which always form the tail and whose
-// order cannot change the VecSum sweep (every TwoSum of two zeros yields the
-// same sum and a +0 error irrespective of order) -- so renorm's output is
-// bit-identical.  Padding slots (i >= m) get key 0 and sink to the end.
+// values (no effect) -- see sort_key for the zeros.
 template <int M>
 MPC_DI void sort_desc(double (&buf)[M], int m) {
   uint64_t key[M];
 #pragma unroll
   for (int i = 0; i < M; i++) key[i] = (i < m) ? sort_key(buf[i]) : 0ull;
   SortNet<M>::apply([&](int a, int b) {
-    bool sw = key[a] < key[b];
-    double va = buf[a], vb = buf[b];
-    uint64_t ka = key[a], kb = key[b];
-    buf[a] = sw ? vb : va;
-    buf[b] = sw ? va : vb;
-    key[a] = sw ? kb : ka;
-    key[b] = sw ? ka : kb;
+    const uint64_t ka = key[a], kb = key[b];
+    key[a] = ka > kb ? ka : kb;
+    key[b] = ka > kb ? kb : ka;
   });
+#pragma unroll
+  for (int i = 0; i < M; i++) buf[i] = from_key(key[i]);
 }
 
 // _vecsum_extract, _kernels.py:81-105, on buf[0..m) (m <= M runtime)
