@@ -211,6 +211,101 @@ MPC_DI bool is_nonoverlapping(const Exp<K>& o) {
   return ok;
 }
 
+// the part of renorm after the sort (VecSum, extraction, repeat pass)
+template <int M, int K>
+MPC_DI Exp<K> renorm_sorted(double (&buf)[M]) {
+  Exp<K> out;
+  vecsum_extract<M, K>(buf, M, out);
+  int it = 0;
+  while (!is_nonoverlapping<K>(out) && it < 6) {
+    double b2[K];
+#pragma unroll
+    for (int i = 0; i < K; i++) b2[i] = out.c[i];
+    vecsum_extract<K, K>(b2, K, out);
+    it++;
+  }
+  return out;
+}
+
+// Structured sort for renorm's term lists: the caller lays buf out as
+// consecutive bands (compile-time sizes B...) that are each sorted by a small
+// network (e.g. exp_mul's magnitude levels), or -- MERGE -- as two sorted
+// runs merged by a merge network.  If the result is not fully sorted (bands
+// overlap, zeros, unnormalized operands) the full network sorts it -- any
+// permutation sorts to the same sequence, so the outcome is always exactly
+// sort_desc's and renorm's bits do not change; the cheap path only has to
+// be right for the common case.
+template <int OFF, int N, typename F>
+MPC_DI void net_at(F&& ce) {
+  SortNet<N>::apply([&](int a, int b) { ce(a + OFF, b + OFF); });
+}
+
+template <int M>
+MPC_DI bool keys_sorted(const uint64_t (&key)[M]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i + 1 < M; i++) ok = ok && key[i] >= key[i + 1];
+  return ok;
+}
+
+// merge networks for two sorted runs of K (positions [0, K) and [K, 2K)),
+// 0-1 verified over all pairs of sorted runs
+template <int K>
+struct MergeNet;
+template <>
+struct MergeNet<3> {
+  template <typename F>
+  MPC_DI static void apply(F&& ce) {
+    ce(2, 3); ce(0, 2); ce(1, 2); ce(2, 4); ce(1, 5); ce(3, 5); ce(1, 2); ce(3, 4);
+  }
+};
+template <>
+struct MergeNet<4> {
+  template <typename F>
+  MPC_DI static void apply(F&& ce) {
+    ce(0, 4); ce(2, 6); ce(2, 4); ce(1, 5); ce(3, 7); ce(3, 5); ce(1, 2); ce(3, 4); ce(5, 6);
+  }
+};
+
+// exp_mul's magnitude bands for k = 3, 4 (see exp_mul): sizes per level
+template <int K>
+struct MulBands;
+template <>
+struct MulBands<3> {  // p00 | e00 p01 p10 | e01 e10 q02 q11 q20 | q12 q21
+  template <typename F>
+  MPC_DI static void apply(F&& ce) {
+    net_at<1, 3>(ce);
+    net_at<4, 5>(ce);
+    net_at<9, 2>(ce);
+  }
+};
+template <>
+struct MulBands<4> {  // p00 | e00 p01 p10 | e01 e10 p02 p11 p20 | e02 e11 e20 q03 q12 q21 q30 | q13 q22 q31
+  template <typename F>
+  MPC_DI static void apply(F&& ce) {
+    net_at<1, 3>(ce);
+    net_at<4, 5>(ce);
+    net_at<9, 7>(ce);
+    net_at<16, 3>(ce);
+  }
+};
+
+template <int M, typename Pre>
+MPC_DI void sort_desc_pre(double (&buf)[M], Pre&& pre) {
+  uint64_t key[M];
+#pragma unroll
+  for (int i = 0; i < M; i++) key[i] = sort_key(buf[i]);
+  auto ce = [&](int a, int b) {
+    const uint64_t ka = key[a], kb = key[b];
+    key[a] = ka > kb ? ka : kb;
+    key[b] = ka > kb ? kb : ka;
+  };
+  pre(ce);
+  if (!keys_sorted<M>(key)) SortNet<M>::apply(ce);
+#pragma unroll
+  for (int i = 0; i < M; i++) buf[i] = from_key(key[i]);
+}
+
 // renorm, _kernels.py:124-139 on buf[0..m) (buf clobbered)
 template <int M, int K>
 MPC_DI Exp<K> renorm(double (&buf)[M], int m) {
@@ -242,7 +337,9 @@ MPC_DI Exp<K> exp_add(const Exp<K>& x, const Exp<K>& y) {
       buf[i] = x.c[i];
       buf[K + i] = y.c[i];
     }
-    return renorm<2 * K, K>(buf, 2 * K);
+    // normalized operands are sorted runs: merge, verify, else full sort
+    sort_desc_pre<2 * K>(buf, [](auto&& ce) { MergeNet<K>::apply(ce); });
+    return renorm_sorted<2 * K, K>(buf);
   }
 }
 
@@ -260,7 +357,8 @@ MPC_DI Exp<K> exp_sub(const Exp<K>& x, const Exp<K>& y) {
       buf[i] = x.c[i];
       buf[K + i] = -y.c[i];
     }
-    return renorm<2 * K, K>(buf, 2 * K);
+    sort_desc_pre<2 * K>(buf, [](auto&& ce) { MergeNet<K>::apply(ce); });
+    return renorm_sorted<2 * K, K>(buf);
   }
 }
 
@@ -272,25 +370,40 @@ MPC_DI Exp<K> exp_mul(const Exp<K>& x, const Exp<K>& y) {
     dd_mul(x.c[0], x.c[1], y.c[0], y.c[1], r.c[0], r.c[1]);
     return r;
   } else {
+    // the reference's term list (_kernels.py:205-219): TwoProd pairs of
+    // levels 0..k-2, plain products of levels k-1 and k.  The order of the
+    // list does not matter to renorm (it sorts), so it is laid out by
+    // magnitude level -- p00 | e00 p01 p10 | ... -- for the banded presort.
     constexpr int M = K * K + K - 1;
+    double p[K - 1][K - 1], e[K - 1][K - 1];
+#pragma unroll
+    for (int s = 0; s < K - 1; s++)
+#pragma unroll
+      for (int i = 0; i < s + 1; i++) two_prod(x.c[i], y.c[s - i], p[s][i], e[s][i]);
     double buf[M];
     int m = 0;
+    buf[m++] = p[0][0];
 #pragma unroll
-    for (int s = 0; s < K - 1; s++) {
+    for (int L = 1; L <= K; L++) {
+      if (L - 1 <= K - 2) {
 #pragma unroll
-      for (int i = 0; i < s + 1; i++) {
-        double p, e;
-        two_prod(x.c[i], y.c[s - i], p, e);
-        buf[m] = p;
-        buf[m + 1] = e;
-        m += 2;
+        for (int i = 0; i < L; i++) buf[m++] = e[L - 1][i];
+      }
+      if (L <= K - 2) {
+#pragma unroll
+        for (int i = 0; i < L + 1; i++) buf[m++] = p[L][i];
+      }
+      if (L == K - 1) {
+#pragma unroll
+        for (int i = 0; i < K; i++) buf[m++] = dmul(x.c[i], y.c[K - 1 - i]);
+      }
+      if (L == K) {
+#pragma unroll
+        for (int i = 1; i < K; i++) buf[m++] = dmul(x.c[i], y.c[K - i]);
       }
     }
-#pragma unroll
-    for (int i = 0; i < K; i++) buf[m++] = dmul(x.c[i], y.c[K - 1 - i]);
-#pragma unroll
-    for (int i = 1; i < K; i++) buf[m++] = dmul(x.c[i], y.c[K - i]);
-    return renorm<M, K>(buf, M);
+    sort_desc_pre<M>(buf, [](auto&& ce) { MulBands<K>::apply(ce); });
+    return renorm_sorted<M, K>(buf);
   }
 }
 
