@@ -1055,7 +1055,10 @@ struct Ops {
       if (e && std::string(e) == "launches") return 0;
       auto kern = panel_cluster_kernel<K>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      const char* cap_s = getenv("MPC_PANEL_CLUSTER");  // cap (experiments)
+      const int cap = cap_s ? atoi(cap_s) : 16;
       for (int c : {16, 8, 4, 2}) {
+        if (c > cap) continue;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(c);
         cfg.blockDim = dim3(PanelCluster<K>::NT);
