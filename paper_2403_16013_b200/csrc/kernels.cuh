@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(PNT) panel_step_kernel(View A, int64_t n, int6
 template <int K>
 struct PanelCluster {
   static constexpr int NT = 256;                    // threads per CTA
-  static constexpr int WMAX = 8;                    // base panel width
+  static constexpr int WMAX = K == 2 ? 8 : 4;       // base panel width (registers: k limbs x 4 arrays)
 };
 
 template <int K>
