@@ -1,0 +1,126 @@
+"""Known-answer cases of the reference's own unit tests,
+restated for the device path: exact integer and exact-rational GEMMs, hand
+LU / TRSM / solve cases, singular detection columns, pivot invariants,
+thread invariance and K = n equivalence.  Values are elementary facts
+(e.g. [[1,2],[3,4]] [[5,6],[7,8]] = [[19,22],[43,50]]), checked exactly."""
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mp():
+    import paper_2403_16013_b200 as m
+
+    m._lib.require_device()
+    return m
+
+
+def frac(x):
+    """exact value of a k-limb expansion given as a sequence of doubles"""
+    return sum((Fraction(float(c)) for c in x), Fraction(0))
+
+
+@pytest.mark.parametrize("kern", ["naive", "blocked"])
+def test_exact_integer_gemm(mp, kern):
+    A = mp.RealMatrix.from_float64(np.array([[1.0, 2.0], [3.0, 4.0]]), 2)
+    B = mp.RealMatrix.from_float64(np.array([[5.0, 6.0], [7.0, 8.0]]), 2)
+    C = mp.rgemm_naive(A, B) if kern == "naive" else mp.rgemm_blocked(A, B)
+    assert np.array_equal(C.data[0], [[19.0, 22.0], [43.0, 50.0]])
+    assert not C.data[1].any()
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_gemm_vs_exact_rational(mp, k):
+    """8x8 products against Fraction arithmetic: |C - AB| <= 8 * 4 eps |A||B|."""
+    rng = np.random.default_rng(7 + k)
+    A = mp.random_matrix(8, 8, k, rng)
+    B = mp.random_matrix(8, 8, k, rng)
+    C = mp.rgemm_blocked(A, B)
+    eps = Fraction(mp.eps_for(k))
+    for i in range(8):
+        for j in range(8):
+            exact = sum(frac(A.data[:, i, t]) * frac(B.data[:, t, j]) for t in range(8))
+            bound = 8 * 4 * eps * sum(abs(frac(A.data[:, i, t]) * frac(B.data[:, t, j]))
+                                      for t in range(8))
+            assert abs(frac(C.data[:, i, j]) - exact) <= bound
+
+
+def test_identity_lu(mp):
+    I = mp.PlanarComplexMatrix.identity(5, 2)
+    f = mp.lu_normal(I)
+    assert f.packed.bitwise_equal(I)
+    assert np.array_equal(f.pivots, np.arange(5))
+
+
+def test_hand_2x2_lu(mp):
+    A = mp.PlanarComplexMatrix(mp.RealMatrix.from_float64(np.array([[1.0, 2.0], [3.0, 4.0]]), 2),
+                               mp.RealMatrix.zeros(2, 2, 2))
+    f = mp.lu_normal(A)
+    assert list(f.pivots) == [1, 1]           # |3| > |1|: the rows swap
+    u = f.packed.re_plane.data
+    eps = Fraction(mp.eps_for(2))
+    assert frac(u[:, 0, 0]) == 3 and frac(u[:, 0, 1]) == 4
+    assert abs(frac(u[:, 1, 0]) - Fraction(1, 3)) <= 2 * eps
+    assert abs(frac(u[:, 1, 1]) - Fraction(2, 3)) <= 4 * eps
+    assert not f.packed.im_plane.data.any()
+
+
+def test_trsm_identity_and_hand(mp):
+    rng = np.random.default_rng(3)
+    L = mp.PlanarComplexMatrix.identity(6, 2)
+    X0 = mp.PlanarComplexMatrix(mp.random_matrix(6, 6, 2, rng), mp.random_matrix(6, 6, 2, rng))
+    assert mp.trsm_unit_lower(L, X0).bitwise_equal(X0)
+    L2 = mp.PlanarComplexMatrix.identity(2, 2)
+    L2.re_plane.data[0, 1, 0] = 2.0
+    b = mp.PlanarComplexMatrix(mp.RealMatrix.from_float64(np.array([[1.0], [0.0]]), 2),
+                               mp.RealMatrix.zeros(2, 1, 2))
+    X = mp.trsm_unit_lower(L2, b)
+    assert X.re_plane.data[0, 0, 0] == 1.0 and X.re_plane.data[0, 1, 0] == -2.0
+    assert not X.im_plane.data.any()
+
+
+def test_solve_identity_and_hand(mp):
+    rng = np.random.default_rng(5)
+    I = mp.PlanarComplexMatrix.identity(7, 2)
+    f = mp.lu_normal(I)
+    b = mp.ComplexVector(np.zeros((2, 7)), np.zeros((2, 7)))
+    b.re[0] = rng.random(7)
+    b.im[0] = rng.random(7)
+    assert mp.solve(f, b).bitwise_equal(b)
+    A = mp.PlanarComplexMatrix.from_complex128(np.array([[1.0, 1.0], [0.0, 1.0]]), 2)
+    bb = mp.ComplexVector(np.zeros((2, 2)), np.zeros((2, 2)))
+    bb.re[0] = [4.0, 3.0]
+    bb.im[0] = [6.0, 4.0]
+    x = mp.solve(mp.lu_normal(A), bb)
+    assert list(x.re[0]) == [1.0, 3.0] and list(x.im[0]) == [2.0, 4.0]
+    assert not x.re[1].any() and not x.im[1].any()
+
+
+def test_singular_columns(mp):
+    with pytest.raises(mp.SingularMatrixError, match="column 0"):
+        mp.lu_normal(mp.PlanarComplexMatrix.zeros(4, 4, 2))
+    base = np.array([[1.0, 2.0, 1.0], [2.0, 4.0, 0.0], [3.0, 6.0, 2.0]])
+    A = mp.PlanarComplexMatrix(mp.RealMatrix.from_float64(base, 2), mp.RealMatrix.zeros(3, 3, 2))
+    with pytest.raises(mp.SingularMatrixError, match="column 1"):
+        mp.lu_normal(A)
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_pivot_invariants_threads_and_K(mp, k):
+    rng = np.random.default_rng(11 + k)
+    n = 48
+    A = mp.PlanarComplexMatrix(mp.random_matrix(n, n, k, rng), mp.random_matrix(n, n, k, rng))
+    f1 = mp.lu_blocked(A, 16, threads=1)
+    f8 = mp.lu_blocked(A, 16, threads=8)
+    assert np.array_equal(f1.pivots, f8.pivots) and f1.packed.bitwise_equal(f8.packed)
+    assert np.all(f1.pivots >= np.arange(n))
+    f4 = mp.lu_blocked(A, 16, kc=mp.KernelChoice(method="4m"))
+    assert np.array_equal(f1.pivots, f4.pivots)           # 3M / 4M: same pivots
+    fn = mp.lu_normal(A)
+    fK = mp.lu_blocked(A, n)
+    assert np.array_equal(fn.pivots, fK.pivots) and fn.packed.bitwise_equal(fK.packed)
