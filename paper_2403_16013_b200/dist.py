@@ -87,9 +87,14 @@ class Layout:
 
 
 class CudaBackend:
-    """Product backend: libmpcb200 on device pointers, current torch stream."""
+    """Product backend: libmpcb200 on device pointers, current torch stream.
+    real_kernel="ozaki": the trailing update through the Ozaki scheme on the
+    INT8 tensor cores (lu_blocked with KernelChoice(real_kernel="ozaki")) --
+    column ranges of that update are independent too (right-operand grids
+    per column, left-operand grids per row of L21), so the distributed
+    result stays bit-identical to the 1-GPU one."""
 
-    def __init__(self, k, method, device):
+    def __init__(self, k, method, device, real_kernel="blocked", d=None, split_bits=None):
         import torch
 
         from . import _lib
@@ -100,6 +105,9 @@ class CudaBackend:
         self.device = device
         self.L = _lib.lib()
         self._lib = _lib
+        self.ozaki = real_kernel == "ozaki"
+        self.d = d if d is not None else {2: 6, 3: 8, 4: 12}[k]   # cmatrix.py:26
+        self.split_bits = split_bits or 0
 
     def _p(self, t, off):
         return t.data_ptr() + 8 * off
@@ -132,6 +140,13 @@ class CudaBackend:
 
     def gemm_sub(self, A, B, C, m, kin, l):
         if m <= 0 or l <= 0:
+            return
+        if self.ozaki:
+            self._lib.check(self.L.mpc_cgemm_ozaki(
+                self.k, self.meth, m, kin, l, self._p(A.re, A.off), self._p(A.im, A.off), A.ld,
+                A.ps, self._p(B.re, B.off), self._p(B.im, B.off), B.ld, B.ps,
+                self._p(C.re, C.off), self._p(C.im, C.off), C.ld, C.ps, self.d, self.split_bits,
+                1, self._st()), "cgemm_ozaki")
             return
         self._lib.check(self.L.mpc_cgemm(
             self.k, self.meth, m, kin, l, self._p(A.re, A.off), self._p(A.im, A.off), A.ld, A.ps,
@@ -294,7 +309,7 @@ class TorchComm:
         return self.dist.broadcast(t, src, async_op=True)
 
 
-def lu_blocked_distributed(re, im, K, method="3m", lookahead=True):
+def lu_blocked_distributed(re, im, K, method="3m", lookahead=True, real_kernel="blocked"):
     """Public multi-GPU entry point: factor a (k, n, n) host matrix over all
     ranks of the default process group (one CUDA device per rank, NCCL).
     Every rank passes the same host arrays (each copies only its own block
@@ -311,7 +326,7 @@ def lu_blocked_distributed(re, im, K, method="3m", lookahead=True):
     loc_re = torch.from_numpy(lay.scatter(re)).to(dev)
     loc_im = torch.from_numpy(lay.scatter(im)).to(dev)
     piv = torch.arange(n, dtype=torch.int64, device=dev)
-    be = CudaBackend(k, method, dev)
+    be = CudaBackend(k, method, dev, real_kernel)
     dist_getrf(be, TorchComm(dist), lay, k, loc_re, loc_im, piv, lookahead)
     return gather_factors(lay, loc_re, loc_im, piv, re.shape)
 
@@ -362,7 +377,7 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
     src_im = torch.from_numpy(lay.scatter(im0)).to(dev)
     loc_re, loc_im = torch.empty_like(src_re), torch.empty_like(src_im)
     piv = torch.empty(n, dtype=torch.int64, device=dev)
-    be = CudaBackend(k, args.method, dev)
+    be = CudaBackend(k, args.method, dev, getattr(args, "real_kernel", "blocked"))
     comm = TorchComm(dist)
 
     def step():
@@ -404,7 +419,8 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record()
-        res = lu_blocked_distributed(re0, im0, K, args.method)
+        res = lu_blocked_distributed(re0, im0, K, args.method,
+                                     real_kernel=getattr(args, "real_kernel", "blocked"))
         a1.record()
         torch.cuda.synchronize()
         te = torch.tensor([a0.elapsed_time(a1)], device=dev)

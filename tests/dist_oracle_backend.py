@@ -19,9 +19,10 @@ def _view(t, off, shape, ld, ps):
 
 
 class OracleBackend:
-    def __init__(self, k, method):
+    def __init__(self, k, method, real_kernel="blocked"):
         self.k = k
         self.method = method
+        self.ozaki = real_kernel == "ozaki"
 
     def empty(self, shape, dtype="f64"):
         return torch.zeros(shape, dtype=torch.float64 if dtype == "f64" else torch.int64)
@@ -75,7 +76,14 @@ class OracleBackend:
         ai = _view(A.im, A.off, (k, m, kin), A.ld, A.ps)
         br = _view(B.re, B.off, (k, kin, l), B.ld, B.ps)
         bi = _view(B.im, B.off, (k, kin, l), B.ld, B.ps)
-        pr, pi = orc.cgemm(ar, ai, br, bi, self.method)
+        if self.ozaki:
+            from oracle import ozaki_ref
+
+            pr, pi = ozaki_ref.cgemm(np.ascontiguousarray(ar), np.ascontiguousarray(ai),
+                                     np.ascontiguousarray(br), np.ascontiguousarray(bi),
+                                     self.method, {2: 6, 3: 8, 4: 12}[k])
+        else:
+            pr, pi = orc.cgemm(ar, ai, br, bi, self.method)
         cr = _view(C.re, C.off, (k, m, l), C.ld, C.ps)
         ci = _view(C.im, C.off, (k, m, l), C.ld, C.ps)
         cr[...] = orc.mat_sub(np.ascontiguousarray(cr), pr)

@@ -93,3 +93,72 @@ def test_distributed_schedule_bitwise(world, case):
         p.join(timeout=300)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) == "ok"
+
+
+def _worker_ozaki(rank, world, port, case, q):
+    """world-size w vs world-size 1 with the Ozaki trailing update: the
+    column distribution must not change a bit (the Ozaki oracle itself is
+    pinned to the reference's golden vectors in test_ozaki.py)."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    from dist_oracle_backend import OracleBackend
+    from oracle import oracle as orc
+    from paper_2403_16013_b200 import problems
+    from paper_2403_16013_b200.dist import Layout, TorchComm, dist_getrf
+
+    orc.set_threads(1)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, K, k, method = case
+        re, im = problems.lu_matrix(n, k, 7 + n, populate_lower=k > 2, renorm=orc.renorm_planes)
+        outs = []
+        for w, rk in ((world, rank), (1, 0)):
+            lay = Layout(n, K, w, rk)
+            lr = torch.from_numpy(lay.scatter(re))
+            li = torch.from_numpy(lay.scatter(im))
+            piv = torch.arange(n, dtype=torch.int64)
+            if w == 1:
+                class Solo:
+                    def broadcast(self, t, src):
+                        return None
+                comm = Solo()
+            else:
+                comm = TorchComm(dist)
+            dist_getrf(OracleBackend(k, method, "ozaki"), comm, lay, k, lr, li, piv, True)
+            outs.append((lay, lr.numpy(), li.numpy(), piv.numpy()))
+        objs = [None] * world
+        dist.all_gather_object(objs, (rank, outs[0][1], outs[0][2], outs[0][3]))
+        if rank == 0:
+            fr, fi = np.zeros_like(re), np.zeros_like(im)
+            for r, a, b, _ in objs:
+                L = Layout(n, K, world, r)
+                L.gather_into(fr, a)
+                L.gather_into(fi, b)
+            _, sr, si, sp = outs[1]
+            ok = all(np.array_equal(o[3], sp) for o in objs)
+            ok = ok and fr.tobytes() == sr.tobytes() and fi.tobytes() == si.tobytes()
+            q.put("ok" if ok else "mismatch")
+    except Exception as e:  # pragma: no cover
+        q.put(f"error on rank {rank}: {e!r}")
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", [(36, 8, 2, "3m"), (30, 7, 2, "4m")])
+def test_distributed_schedule_ozaki(case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_ozaki, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) == "ok"

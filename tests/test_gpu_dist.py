@@ -41,7 +41,8 @@ def _worker(rank, world, port, backend, case, q):
     torch.cuda.set_device(0)
     dist.init_process_group(backend, rank=rank, world_size=world)
     try:
-        n, K, k, method = case
+        n, K, k, method = case[:4]
+        rk = case[4] if len(case) > 4 else "blocked"
         re, im = problems.lu_matrix(n, k, 11, populate_lower=k > 2,
                                     renorm=pkg.renorm_planes if k > 2 else None)
         dev = torch.device("cuda", 0)
@@ -49,7 +50,7 @@ def _worker(rank, world, port, backend, case, q):
         lr = torch.from_numpy(lay.scatter(re)).to(dev)
         li = torch.from_numpy(lay.scatter(im)).to(dev)
         piv = torch.arange(n, dtype=torch.int64, device=dev)
-        dist_getrf(CudaBackend(k, method, dev), TorchComm(dist), lay, k, lr, li, piv, True)
+        dist_getrf(CudaBackend(k, method, dev, rk), TorchComm(dist), lay, k, lr, li, piv, True)
         torch.cuda.synchronize()
         objs = [None] * world
         dist.all_gather_object(objs, (rank, lr.cpu().numpy(), li.cpu().numpy(), piv.cpu().numpy()))
@@ -60,7 +61,7 @@ def _worker(rank, world, port, backend, case, q):
                 L.gather_into(fr, a)
                 L.gather_into(fi, b)
             f = pkg.lu_blocked(pkg.PlanarComplexMatrix(pkg.RealMatrix(re), pkg.RealMatrix(im)), K,
-                               kc=pkg.KernelChoice(method=method))
+                               kc=pkg.KernelChoice(method=method, real_kernel=rk))
             ok = all(np.array_equal(o[3], f.pivots) for o in objs)
             ok = ok and fr.tobytes() == f.packed.re_plane.data.tobytes()
             ok = ok and fi.tobytes() == f.packed.im_plane.data.tobytes()
@@ -77,6 +78,8 @@ def _worker(rank, world, port, backend, case, q):
     (2, "gloo", (300, 64, 2, "3m")),
     (2, "gloo", (257, 48, 2, "4m")),
     (2, "gloo", (96, 32, 3, "3m")),
+    (1, "nccl", (300, 64, 2, "3m", "ozaki")),
+    (2, "gloo", (257, 48, 2, "4m", "ozaki")),
 ])
 def test_dist_cuda_backend_bitwise(world, backend, case):
     ctx = mp.get_context("spawn")
