@@ -54,8 +54,16 @@ constexpr int BM = 128;     // MMA M (one TMEM lane per output row)
 constexpr int BKB = 64;     // K bytes per pipeline stage = 2 MMAs of K = 32
 constexpr int NSL = 3;      // digit slices per part
 constexpr int NGRP = 5;     // accumulator groups s = i + j
-constexpr int NEPI = 16;    // epilogue warps (4 per TMEM lane quadrant)
-constexpr int NTHR = (NEPI + 2) * 32;  // + producer warp + MMA warp
+// epilogue warps: 4 per TMEM lane quadrant (16); 12 for DD (-DMPC_OZAKI_DD_NEPI=12,
+// 3 column groups of 16, 128 registers) measured 1.5% slower at the LU shape
+#ifndef MPC_OZAKI_DD_NEPI
+#define MPC_OZAKI_DD_NEPI 16
+#endif
+template <int KL>
+struct Epi {
+  static constexpr int NEPI = KL == 2 ? MPC_OZAKI_DD_NEPI : 16;
+  static constexpr int NTHR = (NEPI + 2) * 32;  // + producer warp + MMA warp
+};
 constexpr int MAXPAIRS = 160;
 constexpr uint32_t TCOLS = 512;        // two accumulator buffers at columns 0 / 256
 
@@ -256,8 +264,9 @@ MPC_DI void acc_insert(Exp<KL>& c, double q) {
 // warp 17 MMA issuer (one lane).  Pipelines: smem ring full/empty (bulk copy
 // -> MMA -> tcgen05.commit), TMEM double buffer full/empty (MMA -> epilogue).
 template <int KL, int CN, int SB>
-__global__ void __launch_bounds__(NTHR, 1) ozaki_tc_kernel(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(Epi<KL>::NTHR, 1) ozaki_tc_kernel(const __grid_constant__ Params P) {
   using T = Tile<KL>;
+  constexpr int NEPI = Epi<KL>::NEPI;
   constexpr int BN = T::BN, S = T::STAGES;
   constexpr int NCG = NEPI / 4, CPT = BN / NCG;  // column groups, columns per thread
   constexpr int CW = CPT % 8 == 0 ? 8 : 4;       // TMEM load width (x8 or x4)
@@ -642,7 +651,7 @@ void launch_cn(const Params& P, cudaStream_t st, double ops) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = CN == 1 ? dim3((unsigned)((P.Lp / T::BN) * (P.Mp / BM)))
                         : dim3((unsigned)(P.Lp / T::BN), (unsigned)(P.Mp / BM));
-  cfg.blockDim = dim3(NTHR);
+  cfg.blockDim = dim3(Epi<KL>::NTHR);
   cfg.dynamicSmemBytes = T::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
