@@ -34,6 +34,8 @@ inline const mpc::OpsTable* table_for(int k) {
     case 2: return mpc::ops_k2();
     case 3: return mpc::ops_k3();
     case 4: return mpc::ops_k4();
+    case 5: return mpc::ops_k5();  // verification kernels (GEMM / elementwise only)
+    case 6: return mpc::ops_k6();
     default: return nullptr;
   }
 }
@@ -148,7 +150,10 @@ struct WsHolder {
   }
 };
 
-inline bool bad_k(int k) { return table_for(k) == nullptr; }
+// k = 2, 3, 4: every entry point; k = 5, 6 (the k + 2 verification
+// kernels): mat_add, renorm_planes, rgemm and the 4M cgemm
+inline bool bad_k(int k) { return k < 2 || k > 4; }
+inline bool bad_k_gemm(int k) { return table_for(k) == nullptr; }
 inline bool bad_method(int m) { return m != 3 && m != 4; }
 
 #define MPC_TRY try {

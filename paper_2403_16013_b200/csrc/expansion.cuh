@@ -338,8 +338,13 @@ MPC_DI Exp<K> exp_add(const Exp<K>& x, const Exp<K>& y) {
       buf[K + i] = y.c[i];
     }
     // normalized operands are sorted runs: merge, verify, else full sort
-    sort_desc_pre<2 * K>(buf, [](auto&& ce) { MergeNet<K>::apply(ce); });
-    return renorm_sorted<2 * K, K>(buf);
+    // (k > 4: the verification kernels only, plain renorm)
+    if constexpr (K <= 4) {
+      sort_desc_pre<2 * K>(buf, [](auto&& ce) { MergeNet<K>::apply(ce); });
+      return renorm_sorted<2 * K, K>(buf);
+    } else {
+      return renorm<2 * K, K>(buf, 2 * K);
+    }
   }
 }
 
@@ -357,8 +362,12 @@ MPC_DI Exp<K> exp_sub(const Exp<K>& x, const Exp<K>& y) {
       buf[i] = x.c[i];
       buf[K + i] = -y.c[i];
     }
-    sort_desc_pre<2 * K>(buf, [](auto&& ce) { MergeNet<K>::apply(ce); });
-    return renorm_sorted<2 * K, K>(buf);
+    if constexpr (K <= 4) {
+      sort_desc_pre<2 * K>(buf, [](auto&& ce) { MergeNet<K>::apply(ce); });
+      return renorm_sorted<2 * K, K>(buf);
+    } else {
+      return renorm<2 * K, K>(buf, 2 * K);
+    }
   }
 }
 
@@ -402,8 +411,12 @@ MPC_DI Exp<K> exp_mul(const Exp<K>& x, const Exp<K>& y) {
         for (int i = 1; i < K; i++) buf[m++] = dmul(x.c[i], y.c[K - i]);
       }
     }
-    sort_desc_pre<M>(buf, [](auto&& ce) { MulBands<K>::apply(ce); });
-    return renorm_sorted<M, K>(buf);
+    if constexpr (K <= 4) {
+      sort_desc_pre<M>(buf, [](auto&& ce) { MulBands<K>::apply(ce); });
+      return renorm_sorted<M, K>(buf);
+    } else {
+      return renorm<M, K>(buf, M);
+    }
   }
 }
 

@@ -18,8 +18,8 @@ all explicit:
   names; ``strassen`` is rejected as in cmatrix.KernelChoice;
 * ``fp64_pct`` is the algorithmic FP64 op count of the factorization (op
   model v1, DESIGN.md §3) over the measured FP64 peak, for the EFT kernel;
-  ``bwd_err`` is the O(n^2) normwise backward-error probe (DD; nan for
-  TD/QD, whose k + 2 exceeds the kernels built here); ``pivots_equal``
+  ``bwd_err`` is the O(n^2) normwise backward-error probe at k + 2
+  components (the k = 5, 6 verification kernels for TD / QD); ``pivots_equal``
   says whether every repetition produced the same pivot vector.
 
 No CPU fallback: every number comes from the CUDA library.
@@ -268,8 +268,7 @@ def run_bench(cfg):
                     ops = _factor_ops(cfg.n, K, k, cfg.method, cfg.algorithm == "normal")
                     rec.fp64_pct = 100.0 * ops / med / _fp64_peak()
                 rec.pivots_equal = all(np.array_equal(p, pivs[0]) for p in pivs)
-                if k == 2:  # the probe evaluates at k + 2 = 4 (the widest kernel here)
-                    rec.bwd_err = float(backward_error_probe(factors, system.A))
+                rec.bwd_err = float(backward_error_probe(factors, system.A))  # at k + 2
                 if cfg.verify and rec.bwd_err > 10.0 * cfg.n * 2.0 ** (-52 * k):
                     rec.status = "verify_failed"
             records.append(rec)

@@ -260,19 +260,22 @@ def _promote(M, k_new):
 
 def reconstruction_error(f, A, threads=8, extra=2):
     """max componentwise |PA - LU| over both planes (lu.py:236-250), with the
-    L U product at k + extra components through the GPU kernel.  The device
-    path stops at k = 4, so this is available for DD factors (extra = 2)."""
+    L U product at k + extra components through the GPU kernel: the
+    reference's 3M product up to k + extra = 4, the 4M product of the k = 5, 6
+    verification kernels beyond (at k + 2 components the two
+    differ only far below the metric)."""
     from .cmatrix import cgemm
 
     kk = f.packed.k + extra
-    if kk > 4:
-        raise NotImplementedError("reconstruction at k > 4 is not on the B200 path yet")
+    if kk > 6:
+        raise NotImplementedError("verification kernels stop at k = 6")
     from .rmatrix import mat_sub
 
     PA = _promote(permuted(A, f.pivots), kk)
     L = _promote(f.lower(), kk)
     U = _promote(f.upper(), kk)
-    LU = cgemm(L, U, KernelChoice(method="3m", real_kernel="blocked", threads=threads))
+    LU = cgemm(L, U, KernelChoice(method="3m" if kk <= 4 else "4m", real_kernel="blocked",
+                                  threads=threads))
     dre = mat_sub(PA.re_plane, LU.re_plane)
     dim = mat_sub(PA.im_plane, LU.im_plane)
     return max(dre.max_abs(), dim.max_abs())
@@ -281,27 +284,29 @@ def reconstruction_error(f, A, threads=8, extra=2):
 def backward_error_probe(f, A, seed=0):
     """O(n^2) estimate of the normwise backward error ||PA - LU|| / ||A||
     (infinity norm, |Re| + |Im| moduli): r = P A v - L (U v) for a seeded
-    random DD vector v, evaluated in quad-double (k + 2 = 4) with the GPU
-    GEMM at l = 1.  Returns ||r|| / (||A|| ||v||), a lower bound of the
-    normwise backward error, for DD factors."""
+    random vector v, evaluated at k + 2 components (DD: the quad-double
+    kernels; TD / QD: the k = 5, 6 verification kernels) with the GPU GEMM at
+    l = 1.  Returns ||r|| / (||A|| ||v||), a lower bound of the normwise
+    backward error."""
     from .cmatrix import cgemm
 
     k, n = f.packed.k, f.n
-    if k != 2:
-        raise NotImplementedError("probe needs k + 2 <= 4")
+    kk = k + 2
+    if kk > 6:
+        raise NotImplementedError("probe needs k + 2 <= 6")
     rng = np.random.Generator(np.random.Philox(key=np.uint64(seed + 12345)))
-    v = np.zeros((2, 4, n, 1))
+    v = np.zeros((2, kk, n, 1))
     v[0, 0, :, 0] = rng.uniform(-1, 1, n)
     v[1, 0, :, 0] = rng.uniform(-1, 1, n)
     V = PlanarComplexMatrix(RealMatrix(v[0]), RealMatrix(v[1]))
     kc = KernelChoice(method="4m")
-    PA = _promote(permuted(A, f.pivots), 4)
+    PA = _promote(permuted(A, f.pivots), kk)
     y3 = cgemm(PA, V, kc)
     del PA
-    U = _promote(f.upper(), 4)
+    U = _promote(f.upper(), kk)
     y1 = cgemm(U, V, kc)
     del U
-    L = _promote(f.lower(), 4)
+    L = _promote(f.lower(), kk)
     y2 = cgemm(L, y1, kc)
     del L
     from .rmatrix import mat_sub

@@ -124,3 +124,44 @@ def test_pivot_invariants_threads_and_K(mp, k):
     fn = mp.lu_normal(A)
     fK = mp.lu_blocked(A, n)
     assert np.array_equal(fn.pivots, fK.pivots) and fn.packed.bitwise_equal(fK.packed)
+
+
+@pytest.mark.parametrize("kk", [5, 6])
+def test_verification_kernels_vs_exact(mp, kk):
+    """The k = 5, 6 verification kernels: 4M complex product
+    against Fraction arithmetic; the 3M path and the LU are not built there."""
+    rng = np.random.default_rng(kk)
+    A = mp.PlanarComplexMatrix(mp.random_matrix(6, 5, 3, rng).promote(kk),
+                               mp.random_matrix(6, 5, 3, rng).promote(kk))
+    B = mp.PlanarComplexMatrix(mp.random_matrix(5, 4, 3, rng).promote(kk),
+                               mp.random_matrix(5, 4, 3, rng).promote(kk))
+    C = mp.cgemm(A, B, mp.KernelChoice(method="4m"))
+    eps = Fraction(2.0 ** (1 - 53 * kk))
+    ar, ai, br, bi = A.re_plane.data, A.im_plane.data, B.re_plane.data, B.im_plane.data
+    for i in range(6):
+        for j in range(4):
+            re = sum(frac(ar[:, i, t]) * frac(br[:, t, j]) - frac(ai[:, i, t]) * frac(bi[:, t, j])
+                     for t in range(5))
+            mag = sum(abs(frac(ar[:, i, t]) * frac(br[:, t, j])) + abs(frac(ai[:, i, t]) * frac(bi[:, t, j]))
+                      for t in range(5))
+            assert abs(frac(C.re_plane.data[:, i, j]) - re) <= 64 * eps * mag
+    with pytest.raises(ValueError):
+        mp.cgemm(A, B, mp.KernelChoice(method="3m"))
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_td_qd_backward_error(mp, k):
+    """BASELINE's TD / QD accuracy criterion: normwise backward error of the
+    factors <= 10 n u (u = 2^-156 / 2^-208), probed at k + 2 components, and
+    the componentwise reconstruction bound 64 eps max|A| (bench.py:259-262)."""
+    from paper_2403_16013_b200 import lu as lum, problems
+
+    n = 96
+    re, im = problems.lu_matrix(n, k, 3, populate_lower=True, renorm=mp.renorm_planes)
+    A = mp.PlanarComplexMatrix(mp.RealMatrix(re), mp.RealMatrix(im))
+    f = mp.lu_blocked(A, 32)
+    u = 2.0 ** {3: -156, 4: -208}[k]
+    be = lum.backward_error_probe(f, A)
+    assert 0 < be <= 10 * n * u, be
+    rec = lum.reconstruction_error(f, A)
+    assert rec <= 64 * mp.eps_for(k) * A.max_abs(), rec
