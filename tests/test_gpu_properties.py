@@ -50,3 +50,18 @@ def test_reconstruction_small():
     f = mp.lu_blocked(A, 32)
     err = mp.lu.reconstruction_error(f, A)
     assert err <= 64 * mp.eps_for(2) * A.max_abs()
+
+
+@pytest.mark.parametrize("k,n,K", [(2, 4096, 256), (3, 1024, 128)])
+def test_ozaki_lu_accuracy(k, n, K):
+    """real_kernel="ozaki" (the INT8 tensor-core path, d = 6 / 8): the
+    factorization meets the same 10 n u backward-error bound as the EFT
+    kernel (the reference's claim that d = 6 / 8 saturate DD / TD accuracy,
+    ozaki.py:11-17), pivots valid, solve accurate."""
+    re, im = problems.lu_matrix(n, k, 2, populate_lower=k > 2,
+                                renorm=mp.renorm_planes if k > 2 else None)
+    A = pc(re, im)
+    f = mp.lu_blocked(A, K, kc=mp.KernelChoice(method="3m", real_kernel="ozaki"))
+    assert np.all(f.pivots >= np.arange(n)) and np.all(f.pivots < n)
+    be = mp.lu.backward_error_probe(f, A)
+    assert be <= 10 * n * U_PREC[k], be
