@@ -290,6 +290,19 @@ struct MulBands<4> {  // p00 | e00 p01 p10 | e01 e10 p02 p11 p20 | e02 e11 e20 q
   }
 };
 
+// exp_div's residual update terms by level (see exp_div): bands of 2, then
+// 3 per lower level, then the last TwoProd error alone
+template <int K>
+struct DivBands {
+  template <typename F>
+  MPC_DI static void apply(F&& ce) {
+    net_at<0, 2>(ce);
+    if constexpr (K >= 2) net_at<2, 3>(ce);
+    if constexpr (K >= 3) net_at<5, 3>(ce);
+    if constexpr (K >= 4) net_at<8, 3>(ce);
+  }
+};
+
 template <int M, typename Pre>
 MPC_DI void sort_desc_pre(double (&buf)[M], Pre&& pre) {
   uint64_t key[M];
@@ -441,17 +454,29 @@ MPC_DI Exp<K> exp_div(const Exp<K>& x, const Exp<K>& y) {
       if (!is_nonzero(qi) || it == K) {
         stop = true;
       } else {
+        // the term list r, -p_i, -e_i (i < k) laid out by magnitude level
+        // -- r0 -p0 | r1 -e0 -p1 | ... | -e_{k-1} -- for the banded presort
+        // (renorm sorts, so the list order is free; same bits)
+        double p[K], e[K];
+#pragma unroll
+        for (int i = 0; i < K; i++) two_prod(qi, y.c[i], p[i], e[i]);
         double buf[3 * K];
+        int m = 0;
+        buf[m++] = r.c[0];
+        buf[m++] = -p[0];
 #pragma unroll
-        for (int i = 0; i < K; i++) buf[i] = r.c[i];
-#pragma unroll
-        for (int i = 0; i < K; i++) {
-          double p, e;
-          two_prod(qi, y.c[i], p, e);
-          buf[K + 2 * i] = -p;
-          buf[K + 2 * i + 1] = -e;
+        for (int L = 1; L < K; L++) {
+          buf[m++] = r.c[L];
+          buf[m++] = -e[L - 1];
+          buf[m++] = -p[L];
         }
-        r = renorm<3 * K, K>(buf, 3 * K);
+        buf[m++] = -e[K - 1];
+        if constexpr (K <= 4) {
+          sort_desc_pre<3 * K>(buf, [](auto&& ce) { DivBands<K>::apply(ce); });
+          r = renorm_sorted<3 * K, K>(buf);
+        } else {
+          r = renorm<3 * K, K>(buf, 3 * K);
+        }
       }
     }
   }
