@@ -567,7 +567,11 @@ __global__ void __launch_bounds__(PNT) panel_step_kernel(View A, int64_t n, int6
 // launches and their last-block atomics per base panel.
 template <int K>
 struct PanelCluster {
-  static constexpr int NT = 256;                    // threads per CTA
+  // threads per CTA / per row: DD keeps one row per thread with all update
+  // columns in registers (2 threads per row measured 15% slower); TD / QD
+  // split a row's update columns over 2 threads (register footprint)
+  static constexpr int NT = K == 2 ? 256 : 512;
+  static constexpr int TPR = K == 2 ? 1 : 2;
   static constexpr int WMAX = K == 2 ? 8 : 4;       // base panel width (registers: k limbs x 4 arrays)
 };
 
@@ -634,32 +638,38 @@ __global__ void __launch_bounds__(PanelCluster<K>::NT, 1)
     panel_cluster_kernel(View A, int64_t n, int64_t c0, int64_t w, int use3m, int64_t* piv,
                          int64_t* status) {
   namespace cg = cooperative_groups;
-  constexpr int NT = PanelCluster<K>::NT;
+  constexpr int NT = PanelCluster<K>::NT, TPR = PanelCluster<K>::TPR;
   cg::cluster_group cluster = cg::this_cluster();
-  const int64_t T = (int64_t)cluster.num_blocks() * NT;
-  const int64_t gt = (int64_t)cluster.block_rank() * NT + threadIdx.x;
+  // TPR threads share a row: each updates W / TPR of the base panel's
+  // columns (smaller register footprint -> more warps to hide the FP64
+  // latency chains); the multiplier l = cdiv(a_ij, a_jj) is computed by
+  // every thread of the row (identical bits), stored by the first one
+  const int64_t T = (int64_t)cluster.num_blocks() * (NT / TPR);
+  const int part = (int)(threadIdx.x % TPR);
+  const int64_t gt = (int64_t)cluster.block_rank() * (NT / TPR) + threadIdx.x / TPR;
   const int64_t cend = c0 + w;
   if (*(volatile int64_t*)status >= 0) return;  // uniform: written only by earlier launches
   {
     Cand<K> c;
     c.row = -1;
     c.v = exp_zero<K>();
-    for (int64_t i = c0 + gt; i < n; i += T) {
-      Cand<K> o = make_cand<K>(A, i, c0);
-      if (cand_better(o, c)) c = o;
-    }
+    if (part == 0)
+      for (int64_t i = c0 + gt; i < n; i += T) {
+        Cand<K> o = make_cand<K>(A, i, c0);
+        if (cand_better(o, c)) c = o;
+      }
     cluster_pick_and_swap<K>(A, c0, c0, cend, piv, status, c);
   }
-  constexpr int W = PanelCluster<K>::WMAX;
+  constexpr int W = PanelCluster<K>::WMAX, WP = W / TPR;
   for (int64_t j = c0; j < cend; j++) {
     if (*(volatile int64_t*)status >= 0) return;  // uniform after the barrier
-    // the pivot row (a_jj and a_jt, t in (j, cend)) in registers, one round trip
+    // the pivot row (a_jj and this thread's a_jt) in registers, one round trip
     const Exp<K> br = ldexp_<K>(A.re + j * A.ld + j, A.ps);
     const Exp<K> bi = ldexp_<K>(A.im + j * A.ld + j, A.ps);
-    Exp<K> ur[W], ui[W];
+    Exp<K> ur[WP], ui[WP];
 #pragma unroll
-    for (int q = 0; q < W; q++) {
-      int64_t t = j + 1 + q;
+    for (int q = 0; q < WP; q++) {
+      int64_t t = j + 1 + part * WP + q;
       if (t < cend) {
         ur[q] = ldexp_<K>(A.re + j * A.ld + t, A.ps);
         ui[q] = ldexp_<K>(A.im + j * A.ld + t, A.ps);
@@ -671,21 +681,23 @@ __global__ void __launch_bounds__(PanelCluster<K>::NT, 1)
     for (int64_t i = j + 1 + gt; i < n; i += T) {
       Exp<K> ar = ldexp_<K>(A.re + i * A.ld + j, A.ps);
       Exp<K> ai = ldexp_<K>(A.im + i * A.ld + j, A.ps);
-      Exp<K> xr[W], xi[W];
+      Exp<K> xr[WP], xi[WP];
 #pragma unroll
-      for (int q = 0; q < W; q++) {
-        int64_t t = j + 1 + q;
+      for (int q = 0; q < WP; q++) {
+        int64_t t = j + 1 + part * WP + q;
         if (t < cend) {
           xr[q] = ldexp_<K>(A.re + i * A.ld + t, A.ps);
           xi[q] = ldexp_<K>(A.im + i * A.ld + t, A.ps);
         }
       }
       Cx<K> l = cdiv(ar, ai, br, bi);
-      stexp_<K>(A.re + i * A.ld + j, A.ps, l.re);
-      stexp_<K>(A.im + i * A.ld + j, A.ps, l.im);
+      if (part == 0) {
+        stexp_<K>(A.re + i * A.ld + j, A.ps, l.re);
+        stexp_<K>(A.im + i * A.ld + j, A.ps, l.im);
+      }
 #pragma unroll
-      for (int q = 0; q < W; q++) {
-        int64_t t = j + 1 + q;
+      for (int q = 0; q < WP; q++) {
+        int64_t t = j + 1 + part * WP + q;
         if (t < cend) {  // independent across q: a_it -= cmul(l, a_jt)
           Cx<K> pr = cmul(use3m != 0, l.re, l.im, ur[q], ui[q]);
           xr[q] = exp_sub(xr[q], pr.re);
@@ -694,7 +706,7 @@ __global__ void __launch_bounds__(PanelCluster<K>::NT, 1)
           stexp_<K>(A.im + i * A.ld + t, A.ps, xi[q]);
         }
       }
-      if (j + 1 < cend) {  // candidate of the next column from the fresh value
+      if (part == 0 && j + 1 < cend) {  // candidate of the next column from the fresh value
         Cand<K> o;
         o.v = exp_add(exp_abs(xr[0]), exp_abs(xi[0]));
         o.row = exp_greater(o.v, exp_zero<K>()) ? i : -1;
@@ -1089,7 +1101,9 @@ struct Ops {
     if (int csmax = panel_cluster_size()) {
       // smallest power-of-two cluster giving every thread at most one row
       int cs = 1;
-      while (cs < csmax && (int64_t)cs * PanelCluster<K>::NT < n - c0) cs *= 2;
+      while (cs < csmax &&
+             (int64_t)cs * (PanelCluster<K>::NT / PanelCluster<K>::TPR) < n - c0)
+        cs *= 2;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs);
       cfg.blockDim = dim3(PanelCluster<K>::NT);
