@@ -396,6 +396,11 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
 
         clocks = ClockSampler(dev.index)
         clocks.start()
+    from . import device as _dev
+
+    ozaki = getattr(args, "real_kernel", "blocked") == "ozaki"
+    peak = _dev.int8_peak() if ozaki else _dev.fp64_peak()
+    _lib.prof_enable(True, classes=["gemm"])  # the dominant kernel's launches, this rank
     l0 = _lib.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -404,6 +409,15 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
         step()
     e1.record()
     torch.cuda.synchronize()
+    g_ms, g_ops, g_cnt = _lib.prof_summary()["gemm"]
+    _lib.prof_enable(False)
+    ach = g_ops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+    roof = {"bound": "tensor" if ozaki else "fp64", "achieved": ach, "peak": peak / 1e12,
+            "frac": ach * 1e12 / peak,
+            "unit": "TOP/s (INT8 tensor-core ops)" if ozaki else "TFLOP/s (FP64 instr/s)",
+            "traffic": None, "launches": g_cnt,
+            "kernel": "ozaki_tc_kernel" if ozaki else "gemm_kernel<K=2,MODE_G3> (rank 0)",
+            "peak_source": "measured on this device, this run"}
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dist.barrier()
@@ -446,7 +460,7 @@ def bench_main(args, rank, world, re0, im0, metric, workload):
                           "parallelism": f"1-D block-column-cyclic over {world} GPUs, NCCL "
                                          "panel+pivot broadcast, lookahead 1"},
                "pivots_consistent_across_ranks": consistent, "clocks": clk, "e2e": e2e,
-               "gpu_launches": launches, "roofline": None, "cpu_baseline": None,
+               "gpu_launches": launches, "roofline": roof, "cpu_baseline": None,
                "timing": "CUDA events per rank, max over ranks"}
         print(json.dumps(out), flush=True)
     dist.barrier()
