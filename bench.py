@@ -187,6 +187,24 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------- GPU
 
+def _g3_traffic():
+    """dram read + write bytes of one G3 launch from the committed ncu --set
+    full capture at config 4 (profiles/r1_ncu_gemm_G3_cfg4.txt: the step-0
+    update, m = 15872, n = 512, l = 15360).  Algorithmic bytes of that launch
+    are ~16 GB (C read + write); the excess is A / B panel re-reads that miss
+    L2 -- harmless here: the kernel is FP64-bound, DRAM at ~3% of peak."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_gemm_G3_cfg4.txt")
+    try:
+        vals = {}
+        for line in open(path):
+            parts = line.split()
+            if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                vals[parts[0]] = float(parts[-1]) * 1e9  # Gbyte
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def run_b200(args, rank, world):
     import torch
 
@@ -282,7 +300,7 @@ def run_b200(args, rank, world):
             peak_t = peak / 1e12
             roof = {"bound": "fp64", "achieved": achieved, "peak": peak_t,
                     "unit": "TFLOP/s (FP64 instr/s, DADD/DMUL/DFMA = 1)", "frac": achieved / peak_t,
-                    "traffic": None, "kernel": "gemm_kernel<K=2,MODE_G3> (fused 3M trailing update)",
+                    "traffic": _g3_traffic(), "kernel": "gemm_kernel<K=2,MODE_G3> (fused 3M trailing update)",
                     "launches": g_cnt, "avg_launch_ms": g_ms / max(g_cnt, 1),
                     "peak_source": "measured DADD microbenchmark (mpc_fp64_peak) on this device, "
                                    "this run; nominal 18.6 T/s at 1965 MHz"}
