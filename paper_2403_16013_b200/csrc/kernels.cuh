@@ -57,6 +57,10 @@ MPC_DI void stexp_(double* p, int64_t ps, const Exp<K>& e) {
 }
 
 // --------------------------------------------------------- GEMM family
+// grouped raster: G consecutive row tiles sweep the column tiles together
+#ifndef MPC_GEMM_RASTER_G
+#define MPC_GEMM_RASTER_G 32
+#endif
 enum Mode { MODE_REAL = 0, MODE_G3 = 1, MODE_G4 = 2, MODE_S3 = 3, MODE_S4 = 4 };
 
 template <int MODE>
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
   const int tx = tid % SX, ty = tid / SX;
   // grouped raster: G consecutive row tiles sweep the column tiles together,
   // so one B column panel is reused from L2 by G CTAs in flight
-  constexpr int64_t G = 8;
+  constexpr int64_t G = MPC_GEMM_RASTER_G;
   const int64_t tiles_m = (g.m + BM - 1) / BM, tiles_n = (g.l + BN - 1) / BN;
   const int64_t bid = blockIdx.x;
   const int64_t grp = bid / (G * tiles_n);
