@@ -180,3 +180,18 @@ def test_gpu_int8_peak_measured():
 
     p = device.int8_peak(50000)
     assert 1e15 < p < 1e16
+
+
+@pytest.mark.gpu
+def test_gpu_ozaki_wide_split_fallback(orc):
+    """Widths above the int32 digit regime (here 24 bits, n = 16) run the
+    binary64 seam automatically -- still bit-identical to the restatement."""
+    import paper_2403_16013_b200 as mp
+    from oracle import ozaki_ref as ozr
+
+    rng = np.random.default_rng(21)
+    A = mp.random_matrix(20, 16, 2, rng)
+    B = mp.random_matrix(16, 12, 2, rng)
+    assert mp.split_exactness_bound(16) >= 24
+    got = mp.rgemm_ozaki(A, B, 5, split_bits=24).data
+    assert beq(got, ozr.rgemm(A.data, B.data, 5, split_bits=24))
