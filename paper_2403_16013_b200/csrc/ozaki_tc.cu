@@ -65,6 +65,9 @@ struct Epi {
   static constexpr int NTHR = (NEPI + 2) * 32;  // + producer warp + MMA warp
 };
 constexpr int MAXPAIRS = 160;
+#ifndef SPLIT_SMEM_CAP
+#define SPLIT_SMEM_CAP (72 * 1024)  // split CTAs: up to 3 per SM (200 KB: 2x slower, 36 KB: 20% slower)
+#endif
 constexpr uint32_t TCOLS = 512;        // two accumulator buffers at columns 0 / 256
 
 template <int KL>
@@ -793,7 +796,7 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
       attr = true;
     }
     int NL = 16;  // lines per CTA: as many as fit 200 KB of residual
-    while (NL > 1 && (size_t)NL * (size_t)(n | 1) * KL * 8 > 200 * 1024) NL /= 2;
+    while (NL > 1 && (size_t)NL * (size_t)(n | 1) * KL * 8 > SPLIT_SMEM_CAP) NL /= 2;
     const size_t smem = (size_t)NL * (size_t)(n | 1) * KL * 8;
     split_lines_kernel<KL><<<(unsigned)((R + NL - 1) / NL), 256, smem, st>>>(
         src, ld, ps, trans, R, n, NL, d, width, shift, out, Rp, Kp, TR, stackB, sc);
