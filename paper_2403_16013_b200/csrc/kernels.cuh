@@ -924,6 +924,16 @@ inline void retain_pool() {
 }
 
 inline unsigned cdiv_u(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+// SMs of the current device (read once)
+inline int64_t sm_count() {
+  static int64_t n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return (int64_t)v;
+  }();
+  return n;
+}
 
 template <int K>
 struct Ops {
@@ -970,7 +980,13 @@ struct Ops {
       // BK=16, 1 CTA/SM with 132 regs, 64x32 tile with a 4x2 micro-tile --
       // all slower than 32x32 / BK=8 / 2x2 / 2 CTAs per SM
       (void)variant;
-
+      // grids under one wave (TRSM / panel updates on few columns): 16 x 16
+      // tiles, one element per thread -- 4x the CTAs for the same chains
+      // (each element's operation order does not depend on the tiling)
+      if ((int64_t)cdiv_u(g.l, BN) * (int64_t)cdiv_u(g.m, BM) < 2 * sm_count()) {
+        launch_cfg<MODE, 16, 16, BK, 1, 1, 2>(g, st, cls, ops);
+        return;
+      }
     }
     // K=3,4: 2 CTAs/SM (register cap 128) measured best for config 3
     // (TD 1.13 s / QD 2.31 s vs 1.39 / 3.14 s at 1 CTA/SM; 128-thread tiles

@@ -1,5 +1,5 @@
 """One complex Ozaki GEMM of LU-update shape (m x K) (K x m):
-python tools/one_ozaki_rect.py k method m K [reps]"""
+python tools/one_ozaki_rect.py k method m K [reps [l]]  (l defaults to m)"""
 import os
 import sys
 
@@ -11,6 +11,7 @@ from paper_2403_16013_b200 import _lib, device  # noqa: E402
 
 k, meth, m, K = int(sys.argv[1]), sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+l = int(sys.argv[6]) if len(sys.argv) > 6 else m
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(1)
 def mk(r, c):
@@ -18,8 +19,8 @@ def mk(r, c):
     x[0] = torch.rand((r, c), generator=g, device=dev, dtype=torch.float64) * 2 - 1
     return x
 A = [mk(m, K), mk(m, K)]
-B = [mk(K, m), mk(K, m)]
-C = [mk(m, m), mk(m, m)]
+B = [mk(K, l), mk(K, l)]
+C = [mk(m, l), mk(m, l)]
 device.cgemm_ozaki(*A, *B, *C, method=meth, epilogue=1)
 torch.cuda.synchronize()
 _lib.prof_enable(True)
@@ -32,5 +33,5 @@ torch.cuda.synchronize()
 pr = _lib.prof_summary()
 _lib.prof_enable(False)
 g_ms, g_ops, g_n = pr["gemm"]
-print(f"m={m} K={K} k={k} {meth}: {e0.elapsed_time(e1)/reps:.3f} ms/call; tc {g_ms/g_n:.3f} ms x{g_n//reps} "
+print(f"m={m} K={K} l={l} k={k} {meth}: {e0.elapsed_time(e1)/reps:.3f} ms/call; tc {g_ms/g_n:.3f} ms x{g_n//reps} "
       f"{g_ops/(g_ms*1e-3)/1e15:.2f} POPS; other {pr['other'][0]/reps:.3f} ms/call")
