@@ -7,7 +7,7 @@ One "step" = one blocked LU factorization (lu._factor, lu.py:129-163) of the
 seeded synthetic matrix (problems.py; U(-1,1) Re/Im leading limbs, lower
 limbs 0), restored from a pristine device copy at the start of the step.
 `value` = conventional LU GFLOP/s (8 n^3 / 3 per step) over the timed
-region, inputs resident in HBM (8 GiB > L2, no flush needed); `e2e` = the
+region, inputs resident in HBM (8 GiB at cfg4 > L2, no flush needed); `e2e` = the
 same metric through the public in-place API on pinned host buffers, H2D and
 D2H inside the timed region.  N > 1 runs the 1-D block-column-cyclic
 multi-GPU LU (paper_2403_16013_b200.dist) under torchrun.
@@ -399,7 +399,8 @@ def run_b200(args, rank, world):
         "data": "synthetic (seeded Philox U(-1,1), SURVEY.md 8d)",
         "config": {"workload": workload(args), "n": n, "K": K, "k": k, "method": args.method,
                    "seed": args.seed, "parallelism": "1 GPU",
-                   "l2": "inputs 8 GiB > 126 MB L2, restored from a pristine copy every step"},
+                   "l2": "inputs %.2f GiB > 126 MB L2, restored from a pristine copy every step"
+                         % (2 * k * n * n * 8 / 2**30)},
         "fp64_pct_of_measured_peak": fp64_pct,
         "int8_peak_measured_tops": peak_i8 / 1e12 if peak_i8 else None,
         "fp64_peak_measured_tops": peak / 1e12,
