@@ -22,7 +22,7 @@ LIBDIR = os.path.join(HERE, "lib")
 OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libmpcb200.so")
 
-SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "inst_hik.cu", "abi.cu", "ozaki.cu", "ozaki_tc.cu"]
+SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "inst_k5.cu", "inst_k6.cu", "inst_k8.cu", "abi.cu", "ozaki.cu", "ozaki_tc.cu"]
 HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h", "abi_util.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -30,7 +30,7 @@ DEFAULT_SPLIT_BITS = {2: 19, 3: 21, 4: 18}  # ozaki.py:30
 REAL_KERNELS = ("naive", "blocked", "strassen", "ozaki", "b200")
 METHODS = ("3m", "4m")
 SUPPORTED_K = (2, 3, 4)
-VERIFY_K = (5, 6)   # k + 2 verification kernels: blocked 4M GEMM / elementwise only
+VERIFY_K = (5, 6, 8)   # verification kernels (k + 2, REFERENCE_K = 8): blocked GEMM / elementwise only
 
 _kernel_calls = {name: 0 for name in REAL_KERNELS}
 
@@ -187,7 +187,7 @@ def _cgemm(A, B, kc, method):
     check_threads(kc.threads)
     if kc.real_kernel == "strassen":
         raise NotImplementedError("strassen is outside the B200 hot path (see DESIGN.md)")
-    if not (A.k in VERIFY_K and method == "4m" and kc.real_kernel != "ozaki"):
+    if not (A.k in VERIFY_K and kc.real_kernel != "ozaki"):
         _check_k(A.k)
     k, m, n = A.re_plane.data.shape
     l = B.cols

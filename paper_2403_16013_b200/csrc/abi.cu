@@ -173,7 +173,7 @@ double mpc_fp64_peak(int iters, void* stream) {
 int mpc_mat_add(int k, int64_t rows, int64_t cols, const double* a, int64_t lda, int64_t psa,
                 const double* b, int64_t ldb, int64_t psb, double* c, int64_t ldc, int64_t psc,
                 double sign, void* stream) {
-  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6: verification kernels)");
+  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6, 8: verification kernels)");
   if (rows < 0 || cols < 0) return fail("negative dimension");
   MPC_TRY
   cudaStream_t st = (cudaStream_t)stream;
@@ -192,7 +192,7 @@ int mpc_mat_add(int k, int64_t rows, int64_t cols, const double* a, int64_t lda,
 
 int mpc_renorm_planes(int k, int64_t rows, int64_t cols, double* r, int64_t ld, int64_t ps,
                       void* stream) {
-  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6: verification kernels)");
+  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6, 8: verification kernels)");
   MPC_TRY
   cudaStream_t st = (cudaStream_t)stream;
   Stager sg(st);
@@ -207,7 +207,7 @@ int mpc_renorm_planes(int k, int64_t rows, int64_t cols, double* r, int64_t ld, 
 int mpc_rgemm(int k, int64_t m, int64_t n, int64_t l, const double* a, int64_t lda, int64_t psa,
               const double* b, int64_t ldb, int64_t psb, double* c, int64_t ldc, int64_t psc,
               void* stream) {
-  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6: verification kernels)");
+  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6, 8: verification kernels)");
   if (m < 0 || n < 0 || l < 0) return fail("negative dimension");
   MPC_TRY
   cudaStream_t st = (cudaStream_t)stream;
@@ -227,9 +227,8 @@ int mpc_cgemm(int k, int method, int64_t m, int64_t n, int64_t l, const double* 
               const double* a_im, int64_t lda, int64_t psa, const double* b_re,
               const double* b_im, int64_t ldb, int64_t psb, double* c_re, double* c_im,
               int64_t ldc, int64_t psc, int epilogue, void* stream) {
-  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6: verification kernels)");
+  if (bad_k_gemm(k)) return fail("k must be 2, 3, 4 (or 5, 6, 8: verification kernels)");
   if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
-  if (k > 4 && method == 3) return fail("k = 5, 6 (verification kernels): 4M only");
   if (m < 0 || n < 0 || l < 0) return fail("negative dimension");
   if (epilogue != 0 && epilogue != 1) return fail("epilogue must be 0 or 1");
   MPC_TRY

@@ -36,6 +36,7 @@ inline const mpc::OpsTable* table_for(int k) {
     case 4: return mpc::ops_k4();
     case 5: return mpc::ops_k5();  // verification kernels (GEMM / elementwise only)
     case 6: return mpc::ops_k6();
+    case 8: return mpc::ops_k8();  // REFERENCE_K (bench.py:46)
     default: return nullptr;
   }
 }

@@ -21,6 +21,8 @@
 
 namespace mpc {
 
+constexpr int SORTNET_MAX = 41;  // largest SortNet in sortnet.h
+
 #define MPC_DI __device__ __forceinline__
 
 MPC_DI double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -124,15 +126,30 @@ MPC_DI double from_key(uint64_t k) {
 template <int M>
 MPC_DI void sort_desc(double (&buf)[M], int m) {
   uint64_t key[M];
+  if constexpr (M > SORTNET_MAX) {
+    // k = 8 verification kernels (exp_mul: 71 terms): the reference's own
+    // insertion sort, on the keys in local memory (not unrolled)
+    for (int i = 0; i < m; i++) {
+      const uint64_t v = sort_key(buf[i]);
+      int j = i - 1;
+      while (j >= 0 && key[j] < v) {
+        key[j + 1] = key[j];
+        j--;
+      }
+      key[j + 1] = v;
+    }
+    for (int i = 0; i < M; i++) buf[i] = from_key(i < m ? key[i] : 0ull);
+  } else {
 #pragma unroll
-  for (int i = 0; i < M; i++) key[i] = (i < m) ? sort_key(buf[i]) : 0ull;
-  SortNet<M>::apply([&](int a, int b) {
-    const uint64_t ka = key[a], kb = key[b];
-    key[a] = ka > kb ? ka : kb;
-    key[b] = ka > kb ? kb : ka;
-  });
+    for (int i = 0; i < M; i++) key[i] = (i < m) ? sort_key(buf[i]) : 0ull;
+    SortNet<M>::apply([&](int a, int b) {
+      const uint64_t ka = key[a], kb = key[b];
+      key[a] = ka > kb ? ka : kb;
+      key[b] = ka > kb ? kb : ka;
+    });
 #pragma unroll
-  for (int i = 0; i < M; i++) buf[i] = from_key(key[i]);
+    for (int i = 0; i < M; i++) buf[i] = from_key(key[i]);
+  }
 }
 
 // _vecsum_extract, _kernels.py:81-105, on buf[0..m) (m <= M runtime)

@@ -36,7 +36,9 @@ struct OpsTable {
 const OpsTable* ops_k2();
 const OpsTable* ops_k3();
 const OpsTable* ops_k4();
-const OpsTable* ops_k5();  // verification only: rgemm, 4M cgemm, mat_add, renorm_planes
+// verification only (inst_hik.cuh): rgemm, 3M / 4M cgemm, mat_add, renorm_planes
+const OpsTable* ops_k5();
 const OpsTable* ops_k6();
+const OpsTable* ops_k8();
 
 }  // namespace mpc

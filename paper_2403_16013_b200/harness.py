@@ -11,9 +11,9 @@ all explicit:
 * every record carries six more columns -- ``device, ngpus, gflops_conv,
   fp64_pct, pivots_equal, bwd_err`` -- written after the reference's twelve;
   ``read_csv`` accepts both layouts;
-* ``reference_rhs`` evaluates ``b = A x`` with the 4M complex product at the
-  working precision on the device (the reference widens to k = 8,
-  bench.py:199-213; this package has no k = 8 kernels -- SURVEY.md §8f3);
+* ``reference_rhs`` and the matmul check (``_matmul_check``) run at k = 8
+  (REFERENCE_K) on the device's verification kernels, as the reference
+  (bench.py:199-213, 336-348);
 * ``kernel`` accepts ``"b200"`` (= the EFT kernel) besides the reference's
   names; ``strassen`` is rejected as in cmatrix.KernelChoice;
 * ``fp64_pct`` is the algorithmic FP64 op count of the factorization (op
@@ -29,6 +29,7 @@ import csv
 import hashlib
 import statistics
 import time
+from decimal import Decimal, localcontext
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -36,10 +37,10 @@ import numpy as np
 
 from . import _lib
 from .cmatrix import DEFAULT_SPLITS, KernelChoice, PlanarComplexMatrix, cgemm_4m
-from .expansion import PRECISIONS
+from .expansion import PRECISIONS, REFERENCE_K
 from .lu import (ComplexVector, LinearSystem, SingularMatrixError, backward_error_probe,
                  lu_blocked, lu_normal, max_rel_err, solve)
-from .rmatrix import RealMatrix
+from .rmatrix import RealMatrix, mat_sub
 
 CSV_COLUMNS = ["precision", "algorithm", "method", "kernel", "n", "K", "splits", "threads",
                "rep_median_seconds", "max_relerr", "seed", "status"]   # bench.py:48-61
@@ -167,15 +168,52 @@ class BenchRecord:
 
 
 def reference_rhs(A, x):
-    """b := A x with the 4M complex product at the working precision on the
-    device (the reference widens to k = 8 first, bench.py:199-213)."""
+    """bench.py:199-213: b := A x with every operand widened to k = 8
+    (REFERENCE_K, exact), the 4M product on the k = 8 verification kernels
+    (naive ≡ blocked bitwise), then truncated back to the working precision
+    (truncate = the leading k limbs renormalized, rmatrix.py:75-81)."""
     if x.n != A.cols or x.k != A.k:
         raise ValueError("x does not match A")
     k, n = A.k, A.rows
-    X = PlanarComplexMatrix(RealMatrix(np.ascontiguousarray(x.re.reshape(k, n, 1))),
-                            RealMatrix(np.ascontiguousarray(x.im.reshape(k, n, 1))))
-    B = cgemm_4m(A, X, KernelChoice(method="4m", real_kernel="b200"))
-    return ComplexVector(B.re_plane.data.reshape(k, n).copy(), B.im_plane.data.reshape(k, n).copy())
+    A8 = PlanarComplexMatrix(A.re_plane.promote(REFERENCE_K), A.im_plane.promote(REFERENCE_K))
+    X8 = PlanarComplexMatrix(
+        RealMatrix(np.ascontiguousarray(x.re.reshape(k, n, 1))).promote(REFERENCE_K),
+        RealMatrix(np.ascontiguousarray(x.im.reshape(k, n, 1))).promote(REFERENCE_K))
+    B8 = cgemm_4m(A8, X8, KernelChoice(method="4m", real_kernel="naive"))
+    del A8
+    bre = B8.re_plane.truncate(k)
+    bim = B8.im_plane.truncate(k)
+    return ComplexVector(bre.data.reshape(k, n), bim.data.reshape(k, n))
+
+
+def _matmul_check(A, B, C):
+    """bench.py:336-348: max componentwise relative error of C against the
+    k = 8 product (4M, blocked) on the verification kernels."""
+    A8 = PlanarComplexMatrix(A.re_plane.promote(REFERENCE_K), A.im_plane.promote(REFERENCE_K))
+    B8 = PlanarComplexMatrix(B.re_plane.promote(REFERENCE_K), B.im_plane.promote(REFERENCE_K))
+    R = cgemm_4m(A8, B8, KernelChoice(method="4m", real_kernel="blocked"))
+    worst = 0.0
+    for plane_c, plane_r in ((C.re_plane, R.re_plane), (C.im_plane, R.im_plane)):
+        D = mat_sub(plane_c.promote(REFERENCE_K), plane_r)
+        denom = np.maximum(np.abs(plane_r.data[0]), np.finfo(float).tiny)
+        worst = max(worst, float((np.abs(D.data[0]) / denom).max()))
+    return worst
+
+
+def float_to_string(v, digits=17):
+    """exp_to_string(Expansion.from_float(v, k), digits) (expansion.py:199-215)
+    for a binary64 value: correctly rounded decimal, same formatting."""
+    if v == 0.0:
+        return "0.0"
+    with localcontext() as ctx:
+        ctx.prec = digits
+        d = +Decimal(v)
+    s = str(d)
+    if "E" in s:
+        s = s.replace("E", "e")
+    elif "." not in s:
+        s += ".0"
+    return s
 
 
 def gen_problem(n, seed, precision):
@@ -277,8 +315,8 @@ def run_bench(cfg):
 
 def run_matmul_bench(cfg, check=False):
     """bench.py:283-333: C = A B on two seeded U[0,1) matrices, median of
-    reps per thread count.  (check=True: 3M vs 4M agreement of the real
-    planes, bitwise by construction, cmatrix.py:157-169.)"""
+    reps per thread count; check=True records the componentwise maximum
+    relative error against the k = 8 product (_matmul_check)."""
     cfg.validate()
     _lib.require_device()
     from .cmatrix import cgemm
@@ -299,18 +337,14 @@ def run_matmul_bench(cfg, check=False):
             t0 = time.perf_counter()
             C = cgemm(A, B, kc)
             times.append(time.perf_counter() - t0)
-        status = "ok"
+        err_str = "nan"
         if check:
-            other = KernelChoice(method="4m" if cfg.method == "3m" else "3m",
-                                 real_kernel=cfg.kernel, d=cfg.splits)
-            C2 = cgemm(A, B, other)
-            if C2.re_plane.data.tobytes() != C.re_plane.data.tobytes():
-                status = "verify_failed"
+            err_str = float_to_string(_matmul_check(A, B, C), 17)
         med = statistics.median(times)
         records.append(BenchRecord(precision=_precision_name(k), algorithm="matmul",
                                    method=cfg.method, kernel=cfg.kernel, n=n, K=0, splits=d,
-                                   threads=t, rep_median_seconds=med, max_relerr="nan",
-                                   seed=cfg.seed, status=status, gflops_conv=8.0 * n ** 3 / med / 1e9))
+                                   threads=t, rep_median_seconds=med, max_relerr=err_str,
+                                   seed=cfg.seed, status="ok", gflops_conv=8.0 * n ** 3 / med / 1e9))
     return records
 
 

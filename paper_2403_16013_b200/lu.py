@@ -260,22 +260,20 @@ def _promote(M, k_new):
 
 def reconstruction_error(f, A, threads=8, extra=2):
     """max componentwise |PA - LU| over both planes (lu.py:236-250), with the
-    L U product at k + extra components through the GPU kernel: the
-    reference's 3M product up to k + extra = 4, the 4M product of the k = 5, 6
-    verification kernels beyond (at k + 2 components the two
-    differ only far below the metric)."""
-    from .cmatrix import cgemm
+    L U product at k + extra components through the GPU kernel, 3M blocked as
+    the reference (k + extra in 2..6 or 8: the verification kernels beyond
+    k = 4)."""
+    from .cmatrix import SUPPORTED_K, VERIFY_K, cgemm
 
     kk = f.packed.k + extra
-    if kk > 6:
-        raise NotImplementedError("verification kernels stop at k = 6")
+    if kk not in SUPPORTED_K + VERIFY_K:
+        raise NotImplementedError(f"no kernels at k + extra = {kk} (2..6, 8)")
     from .rmatrix import mat_sub
 
     PA = _promote(permuted(A, f.pivots), kk)
     L = _promote(f.lower(), kk)
     U = _promote(f.upper(), kk)
-    LU = cgemm(L, U, KernelChoice(method="3m" if kk <= 4 else "4m", real_kernel="blocked",
-                                  threads=threads))
+    LU = cgemm(L, U, KernelChoice(method="3m", real_kernel="blocked", threads=threads))
     dre = mat_sub(PA.re_plane, LU.re_plane)
     dim = mat_sub(PA.im_plane, LU.im_plane)
     return max(dre.max_abs(), dim.max_abs())

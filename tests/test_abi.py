@@ -50,10 +50,10 @@ def test_version_and_errors(lib):
     rc = lib.mpc_cgemm(7, 3, 2, 2, 2, *[a.ctypes.data] * 2, 2, 4, *[a.ctypes.data] * 2, 2, 4,
                        *[a.ctypes.data] * 2, 2, 4, 0, None)
     assert rc == _lib.MPC_ERR and "k must be" in _lib.last_error()
-    # k = 5, 6: the verification kernels exist for the 4M product only
-    rc = lib.mpc_cgemm(5, 3, 2, 2, 2, *[a.ctypes.data] * 2, 2, 4, *[a.ctypes.data] * 2, 2, 4,
+    # k = 5, 6, 8: verification kernels (GEMM / elementwise); none at k = 7
+    rc = lib.mpc_cgemm(7, 4, 2, 2, 2, *[a.ctypes.data] * 2, 2, 4, *[a.ctypes.data] * 2, 2, 4,
                        *[a.ctypes.data] * 2, 2, 4, 0, None)
-    assert rc == _lib.MPC_ERR and "4M only" in _lib.last_error()
+    assert rc == _lib.MPC_ERR and "5, 6, 8" in _lib.last_error()
     rc = lib.mpc_getrf(5, 4, 4, 2, a.ctypes.data, a.ctypes.data, a.ctypes.data, None)
     assert rc == _lib.MPC_ERR and "k must be" in _lib.last_error()
     rc = lib.mpc_cgemm(2, 5, 2, 2, 2, *[a.ctypes.data] * 2, 2, 4, *[a.ctypes.data] * 2, 2, 4,

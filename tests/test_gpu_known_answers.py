@@ -126,10 +126,10 @@ def test_pivot_invariants_threads_and_K(mp, k):
     assert np.array_equal(fn.pivots, fK.pivots) and fn.packed.bitwise_equal(fK.packed)
 
 
-@pytest.mark.parametrize("kk", [5, 6])
+@pytest.mark.parametrize("kk", [5, 6, 8])
 def test_verification_kernels_vs_exact(mp, kk):
-    """The k = 5, 6 verification kernels: 4M complex product
-    against Fraction arithmetic; the 3M path and the LU are not built there."""
+    """The k = 5, 6, 8 verification kernels: 4M complex product
+    against Fraction arithmetic, 3M.re == 4M.re bitwise; no LU there."""
     rng = np.random.default_rng(kk)
     A = mp.PlanarComplexMatrix(mp.random_matrix(6, 5, 3, rng).promote(kk),
                                mp.random_matrix(6, 5, 3, rng).promote(kk))
@@ -145,8 +145,10 @@ def test_verification_kernels_vs_exact(mp, kk):
             mag = sum(abs(frac(ar[:, i, t]) * frac(br[:, t, j])) + abs(frac(ai[:, i, t]) * frac(bi[:, t, j]))
                       for t in range(5))
             assert abs(frac(C.re_plane.data[:, i, j]) - re) <= 64 * eps * mag
+    C3 = mp.cgemm(A, B, mp.KernelChoice(method="3m"))
+    assert C3.re_plane.data.tobytes() == C.re_plane.data.tobytes()
     with pytest.raises(ValueError):
-        mp.cgemm(A, B, mp.KernelChoice(method="3m"))
+        mp.lu_blocked(A, 2)
 
 
 @pytest.mark.parametrize("k", [3, 4])
