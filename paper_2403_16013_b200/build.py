@@ -23,7 +23,7 @@ OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libmpcb200.so")
 
 SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "inst_k5.cu", "inst_k6.cu", "inst_k8.cu", "abi.cu", "ozaki.cu", "ozaki_tc.cu"]
-HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h", "abi_util.h"]
+HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h", "abi_util.h", "inst_hik.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

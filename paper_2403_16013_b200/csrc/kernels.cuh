@@ -975,6 +975,12 @@ struct Ops {
   static void gemm_launch(const GemmArgs& g, cudaStream_t st, int cls, double per_elem) {
     if (g.m <= 0 || g.l <= 0) return;
     double ops = (double)g.m * (double)g.l * (double)g.n * per_elem;
+    // matrix-vector products (reference_rhs at k = 8, the backward-error
+    // probe at k + 2): 32 x 1 tiles, no idle columns
+    if (g.l == 1) {
+      launch_cfg<MODE, 32, 1, BK, 1, 1, (K >= 5 ? 1 : 2)>(g, st, cls, ops);
+      return;
+    }
     if constexpr (K == 2) {
       // alternatives measured in round 1 (profiles/r1_gemm_variants.txt):
       // BK=16, 1 CTA/SM with 132 regs, 64x32 tile with a 4x2 micro-tile --
