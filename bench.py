@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--ill", action="store_true", help="row-scaled ill-conditioned input (cfg4 #2)")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-accuracy", action="store_true",
+                   help="skip the forward / backward error report")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-prof", action="store_true")
     p.add_argument("--no-alt", action="store_true",
@@ -341,6 +343,17 @@ def run_b200(args, rank, world):
                "api": "paper_2403_16013_b200.lu.factor_inplace (%s, host pointers)"
                       % ("mpc_getrf_ozaki" if ozaki else "mpc_getrf")}
 
+    # BASELINE accuracy report on the headline factorization (outside the
+    # timed region): forward error of x = solve(b = A (1+1i)) and the
+    # backward-error probe at k + 2 against 10 n u
+    acc = None
+    if not args.no_accuracy:
+        a0 = time.perf_counter()
+        acc = device.accuracy(A0r, A0i, Wr, Wi, piv, args.method, seed=args.seed)
+        torch.cuda.synchronize()
+        acc["seconds"] = time.perf_counter() - a0
+        acc["factor_kernel"] = args.real_kernel
+
     cpu = None
     if not args.no_cpu:
         g, threads, t = cpu_lu_gflops(min(args.cpu_n, n), min(K, args.cpu_n), k, args.method,
@@ -391,6 +404,9 @@ def run_b200(args, rank, world):
                             "kernel": "ozaki_tc_kernel" if alt_kernel == "ozaki" else "gemm_kernel<2,G3>"},
                "note": "KernelChoice(real_kernel=%r): a different reference algorithm (ozaki.py / "
                        "rgemm.py), parity-checked against the reference separately" % alt_kernel}
+        if not args.no_accuracy:
+            alt["accuracy"] = device.accuracy(A0r, A0i, Wr, Wi, apiv, args.method,
+                                              seed=args.seed)
 
     out = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
@@ -406,6 +422,7 @@ def run_b200(args, rank, world):
         "fp64_peak_measured_tops": peak / 1e12,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
         "gpu_launches": int(launches), "breakdown": breakdown, "alt_real_kernel": alt,
+        "accuracy": acc,
     }
     print(json.dumps(out), flush=True)
 

@@ -167,3 +167,38 @@ def test_td_qd_backward_error(mp, k):
     assert 0 < be <= 10 * n * u, be
     rec = lum.reconstruction_error(f, A)
     assert rec <= 64 * mp.eps_for(k) * A.max_abs(), rec
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [2, 3])
+def test_device_accuracy_report(mp, k):
+    """device.accuracy (bench.py's accuracy object) against the host API:
+    same forward error as lu.max_rel_err(solve(f, A (1+1i))), backward-error
+    probe within 10 n u, for DD and TD."""
+    import torch
+
+    from paper_2403_16013_b200 import device, problems
+
+    n, K = 80, 16
+    re, im = problems.lu_matrix(n, k, 5, populate_lower=k > 2,
+                                renorm=mp.renorm_planes if k > 2 else None)
+    A = mp.PlanarComplexMatrix(mp.RealMatrix(re.copy()), mp.RealMatrix(im.copy()))
+    f = mp.lu_blocked(A, K)
+    xt = mp.ComplexVector(np.zeros((k, n)), np.zeros((k, n)))
+    xt.re[0] = 1.0
+    xt.im[0] = 1.0
+    X = mp.PlanarComplexMatrix(mp.RealMatrix(xt.re.reshape(k, n, 1).copy()),
+                               mp.RealMatrix(xt.im.reshape(k, n, 1).copy()))
+    B = mp.cgemm(A, X, mp.KernelChoice(method="4m"))
+    b = mp.ComplexVector(B.re_plane.data.reshape(k, n), B.im_plane.data.reshape(k, n))
+    fwd_host = mp.max_rel_err(mp.solve(f, b), xt)
+
+    dev = torch.device("cuda", 0)
+    Ar, Ai = torch.from_numpy(re).to(dev), torch.from_numpy(im).to(dev)
+    Wr, Wi = Ar.clone(), Ai.clone()
+    piv = torch.empty(n, dtype=torch.int64, device=dev)
+    assert device.getrf(Wr, Wi, piv, K) == -1
+    assert np.array_equal(piv.cpu().numpy(), f.pivots)
+    acc = device.accuracy(Ar, Ai, Wr, Wi, piv)
+    assert acc["fwd_err"] == pytest.approx(fwd_host, rel=1e-12, abs=0.0)
+    assert 0 < acc["bwd_err_probe"] <= acc["bwd_bound_10nu"] and acc["bwd_ok"]
