@@ -372,6 +372,45 @@ int64_t mpc_lu_panel(int k, int method, int64_t n, double* re, double* im, int64
   MPC_CATCH
 }
 
+namespace {
+// pinned (page-locked) host memory: async copies from it do not block the host
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// device-to-host copies of finished row blocks on a copy stream (getrf's
+// RowSink), so that the D2H of the factors overlaps the rest of the LU
+struct RowD2H {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev = nullptr;
+  const double* dr;
+  const double* di;
+  double* hr;
+  double* hi;
+  int k;
+  int64_t n;
+  static void fn(void* c, int64_t r0, int64_t r1, cudaStream_t st) {
+    auto* s = (RowD2H*)c;
+    ck(cudaEventRecord(s->ev, st), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(s->cs, s->ev, 0), "cudaStreamWaitEvent");
+    const size_t bytes = sizeof(double) * (size_t)(r1 - r0) * (size_t)s->n;
+    for (int q = 0; q < s->k; q++) {
+      const size_t off = (size_t)q * s->n * s->n + (size_t)r0 * s->n;
+      ck(cudaMemcpyAsync(s->hr + off, s->dr + off, bytes, cudaMemcpyDeviceToHost, s->cs), "D2H");
+      ck(cudaMemcpyAsync(s->hi + off, s->di + off, bytes, cudaMemcpyDeviceToHost, s->cs), "D2H");
+    }
+  }
+};
+struct SinkGuard {
+  ~SinkGuard() { mpc::row_sink() = mpc::RowSink{nullptr, nullptr}; }
+};
+}  // namespace
+
 int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* im, int64_t* piv,
                   void* stream) {
   if (bad_k(k)) return fail("k must be 2, 3 or 4");
@@ -383,17 +422,44 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
   Stager sg(st);
   if (!sg.classify({re, im, piv})) return MPC_ERR;
   int64_t e = extent(k, n, n, n, n * n);
-  double* dr = sg.map(re, e, true, true);
-  double* di = sg.map(im, e, true, true);
+  // host factors in pinned memory: finished row blocks stream back while
+  // the LU runs (the staged copy-out below then skips them)
+  const bool overlap = sg.host() && n > 0 && is_pinned(re) && is_pinned(im);
+  double* dr = sg.map(re, e, true, !overlap);
+  double* di = sg.map(im, e, true, !overlap);
   int64_t* dp = sg.map(piv, n, false, true);
   int64_t status = -1;
+  RowD2H d2h;
+  SinkGuard guard;
+  if (overlap) {
+    ck(cudaStreamCreateWithFlags(&d2h.cs, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&d2h.ev, cudaEventDisableTiming), "cudaEventCreate");
+    d2h.dr = dr;
+    d2h.di = di;
+    d2h.hr = re;
+    d2h.hi = im;
+    d2h.k = k;
+    d2h.n = n;
+    mpc::row_sink() = mpc::RowSink{RowD2H::fn, &d2h};
+  }
   if (n > 0) {
     iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dp, n);
     WsHolder w(k, n, st);
     table_for(k)->getrf(method == 3, mpc::View{dr, di, n, n * n}, n, K, dp, w.ws, st);
+    mpc::row_sink() = mpc::RowSink{nullptr, nullptr};
     status = w.read_status();
   }
+  if (overlap) {
+    // the staged buffers are freed on st: order it after the copy stream
+    ck(cudaEventRecord(d2h.ev, d2h.cs), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(st, d2h.ev, 0), "cudaStreamWaitEvent");
+  }
   sg.finish();
+  if (overlap) {
+    ck(cudaStreamSynchronize(d2h.cs), "cudaStreamSynchronize");
+    cudaEventDestroy(d2h.ev);
+    cudaStreamDestroy(d2h.cs);
+  }
   return status;
   MPC_CATCH
 }

@@ -452,6 +452,20 @@ struct PanelWs {     // device workspace for the pivot reductions
 
 constexpr int PNT = 256;  // threads per block of the panel kernels
 
+// Host-side hook of getrf: called (on the enqueueing thread) once the work
+// that finalizes rows [r0, r1) of every plane has been enqueued on st --
+// row block b is final after step b's trailing-update enqueue (later steps
+// only swap and update rows >= its end).  The ABI uses it to overlap the
+// device-to-host copy of finished row blocks with the rest of the LU.
+struct RowSink {
+  void (*fn)(void* ctx, int64_t r0, int64_t r1, cudaStream_t st);
+  void* ctx;
+};
+inline RowSink& row_sink() {
+  static thread_local RowSink s{nullptr, nullptr};
+  return s;
+}
+
 // Final stage shared by the pivot kernels: the last block to finish reduces
 // the per-block partials (in block order), records piv[j] and swaps rows j
 // and p inside the active column range [c0, cend) (the other columns are
@@ -1238,7 +1252,10 @@ struct Ops {
       int64_t kw = std::min(Kp, n - jb);
       int64_t end = jb + kw;
       laswp(A, 0, jb, piv, jb, end, st, ws.status);  // left of the panel
-      if (end == n) break;
+      if (end == n) {
+        if (row_sink().fn) row_sink().fn(row_sink().ctx, jb, end, st);
+        break;
+      }
       int64_t kw2 = std::min(Kp, n - end);
       // narrow update of block b+1, then factor it on the side stream
       update_cols(use3m, A, n, jb, kw, end, end + kw2, piv, ws.status, st);
@@ -1250,6 +1267,7 @@ struct Ops {
       mark(sp);
       // rest of panel b's update overlaps the panel factorization
       update_cols(use3m, A, n, jb, kw, end + kw2, n, piv, ws.status, st);
+      if (row_sink().fn) row_sink().fn(row_sink().ctx, jb, end, st);
       mark(st);
       cudaStreamWaitEvent(st, ev_panel, 0);
       mark(st);

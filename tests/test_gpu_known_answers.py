@@ -202,3 +202,32 @@ def test_device_accuracy_report(mp, k):
     acc = device.accuracy(Ar, Ai, Wr, Wi, piv)
     assert acc["fwd_err"] == pytest.approx(fwd_host, rel=1e-12, abs=0.0)
     assert 0 < acc["bwd_err_probe"] <= acc["bwd_bound_10nu"] and acc["bwd_ok"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,n,K", [(2, 300, 64), (3, 130, 32), (2, 64, 64)])
+def test_factor_inplace_pinned_overlap(mp, k, n, K):
+    """Host factors in pinned memory: the C-ABI streams finished row blocks
+    back while the LU runs (RowSink); the result must equal the pageable
+    (staged) path and the device path bit for bit, pivots included."""
+    import torch
+
+    from paper_2403_16013_b200 import lu as lum, problems
+
+    re, im = problems.lu_matrix(n, k, 7, populate_lower=k > 2,
+                                renorm=mp.renorm_planes if k > 2 else None)
+    pr = torch.empty(re.shape, dtype=torch.float64, pin_memory=True)
+    pi = torch.empty(im.shape, dtype=torch.float64, pin_memory=True)
+    pr.numpy()[...] = re
+    pi.numpy()[...] = im
+    pp = lum.factor_inplace(pr.numpy(), pi.numpy(), K)
+    gr, gi = re.copy(), im.copy()
+    gp = lum.factor_inplace(gr, gi, K)
+    dev = torch.device("cuda", 0)
+    dr, di = torch.from_numpy(re).to(dev), torch.from_numpy(im).to(dev)
+    dp = torch.empty(n, dtype=torch.int64, device=dev)
+    lum.factor_inplace(dr, di, K, piv=dp)
+    torch.cuda.synchronize()
+    assert np.array_equal(pp, gp) and np.array_equal(pp, dp.cpu().numpy())
+    assert pr.numpy().tobytes() == gr.tobytes() == dr.cpu().numpy().tobytes()
+    assert pi.numpy().tobytes() == gi.tobytes() == di.cpu().numpy().tobytes()
