@@ -407,7 +407,49 @@ struct RowD2H {
   }
 };
 struct SinkGuard {
-  ~SinkGuard() { mpc::row_sink() = mpc::RowSink{nullptr, nullptr}; }
+  ~SinkGuard() {
+    mpc::row_sink() = mpc::RowSink{nullptr, nullptr};
+    mpc::col_source() = mpc::ColSource{nullptr, nullptr, 0};
+  }
+};
+
+// host-to-device copy of the input in column blocks on the copy stream
+// (getrf's ColSource): block boundaries K, 2K, 2K + 4K, ... match the
+// first panel, the narrow update and step 0's update chunks
+struct ColH2D {
+  std::vector<int64_t> lo;  // first column of each block
+  std::vector<cudaEvent_t> ev;
+  size_t waited = 0;
+  ~ColH2D() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  void issue(cudaStream_t cs, double* dr, double* di, const double* hr, const double* hi, int k,
+             int64_t n, int64_t K, int64_t chunk) {
+    int64_t c = 0;
+    while (c < n) {
+      int64_t w = (c < 2 * K) ? K : chunk;
+      int64_t c1 = std::min(n, c + w);
+      const size_t pitch = sizeof(double) * (size_t)n;
+      for (int q = 0; q < k; q++) {
+        const size_t off = (size_t)q * n * n + (size_t)c;
+        ck(cudaMemcpy2DAsync(dr + off, pitch, hr + off, pitch, sizeof(double) * (size_t)(c1 - c),
+                             (size_t)n, cudaMemcpyHostToDevice, cs), "H2D");
+        ck(cudaMemcpy2DAsync(di + off, pitch, hi + off, pitch, sizeof(double) * (size_t)(c1 - c),
+                             (size_t)n, cudaMemcpyHostToDevice, cs), "H2D");
+      }
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventRecord(e, cs), "cudaEventRecord");
+      lo.push_back(c);
+      ev.push_back(e);
+      c = c1;
+    }
+  }
+  static void need(void* ctx, int64_t c1, cudaStream_t st) {
+    auto* s = (ColH2D*)ctx;
+    while (s->waited < s->ev.size() && s->lo[s->waited] < c1)
+      ck(cudaStreamWaitEvent(st, s->ev[s->waited++], 0), "cudaStreamWaitEvent");
+  }
 };
 }  // namespace
 
@@ -425,15 +467,22 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
   // host factors in pinned memory: finished row blocks stream back while
   // the LU runs (the staged copy-out below then skips them)
   const bool overlap = sg.host() && n > 0 && is_pinned(re) && is_pinned(im);
-  double* dr = sg.map(re, e, true, !overlap);
-  double* di = sg.map(im, e, true, !overlap);
+  double* dr = sg.map(re, e, !overlap, !overlap);
+  double* di = sg.map(im, e, !overlap, !overlap);
   int64_t* dp = sg.map(piv, n, false, true);
   int64_t status = -1;
   RowD2H d2h;
+  ColH2D h2d;
   SinkGuard guard;
   if (overlap) {
     ck(cudaStreamCreateWithFlags(&d2h.cs, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&d2h.ev, cudaEventDisableTiming), "cudaEventCreate");
+    // the copy stream starts after the allocations enqueued on st
+    ck(cudaEventRecord(d2h.ev, st), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(d2h.cs, d2h.ev, 0), "cudaStreamWaitEvent");
+    const int64_t chunk = 4 * K;
+    h2d.issue(d2h.cs, dr, di, re, im, k, n, K, chunk);
+    mpc::col_source() = mpc::ColSource{ColH2D::need, &h2d, chunk};
     d2h.dr = dr;
     d2h.di = di;
     d2h.hr = re;
@@ -447,6 +496,7 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
     WsHolder w(k, n, st);
     table_for(k)->getrf(method == 3, mpc::View{dr, di, n, n * n}, n, K, dp, w.ws, st);
     mpc::row_sink() = mpc::RowSink{nullptr, nullptr};
+    mpc::col_source() = mpc::ColSource{nullptr, nullptr, 0};
     status = w.read_status();
   }
   if (overlap) {

@@ -465,6 +465,19 @@ inline RowSink& row_sink() {
   static thread_local RowSink s{nullptr, nullptr};
   return s;
 }
+// The input side: getrf calls need(ctx, c1, st) before st first touches
+// columns [.., c1) of any row, so the host-to-device copy of later column
+// blocks can still be in flight (step 0's trailing update then runs in
+// column chunks that each wait only for their own columns).
+struct ColSource {
+  void (*need)(void* ctx, int64_t c1, cudaStream_t st);
+  void* ctx;
+  int64_t chunk;  // columns per update chunk at step 0
+};
+inline ColSource& col_source() {
+  static thread_local ColSource s{nullptr, nullptr, 0};
+  return s;
+}
 
 // Final stage shared by the pivot kernels: the last block to finish reduces
 // the per-block partials (in block order), records piv[j] and swaps rows j
@@ -1245,7 +1258,12 @@ struct Ops {
       cudaEventRecord(e, s);
       tev.push_back(e);
     };
+    const ColSource src = col_source();
+    auto need = [&](int64_t c1) {
+      if (src.need) src.need(src.ctx, std::min(c1, n), st);
+    };
     mark(st);
+    need(std::min(Kp, n));
     panel_rec(use3m, A, n, 0, std::min(Kp, n), piv, ws, st);
     mark(st);
     for (int64_t jb = 0; jb < n; jb += Kp) {
@@ -1258,6 +1276,7 @@ struct Ops {
       }
       int64_t kw2 = std::min(Kp, n - end);
       // narrow update of block b+1, then factor it on the side stream
+      if (jb == 0) need(end + kw2);
       update_cols(use3m, A, n, jb, kw, end, end + kw2, piv, ws.status, st);
       cudaEventRecord(ev_narrow, st);
       mark(st);
@@ -1266,7 +1285,17 @@ struct Ops {
       cudaEventRecord(ev_panel, sp);
       mark(sp);
       // rest of panel b's update overlaps the panel factorization
-      update_cols(use3m, A, n, jb, kw, end + kw2, n, piv, ws.status, st);
+      if (jb == 0 && src.need) {
+        // step 0 in column chunks, each behind its own host-to-device copy
+        // (per-column work, so the chunking does not change any bits)
+        const int64_t ch = std::max<int64_t>(src.chunk, Kp);
+        for (int64_t c0 = end + kw2; c0 < n; c0 += ch) {
+          need(c0 + ch);
+          update_cols(use3m, A, n, jb, kw, c0, std::min(n, c0 + ch), piv, ws.status, st);
+        }
+      } else {
+        update_cols(use3m, A, n, jb, kw, end + kw2, n, piv, ws.status, st);
+      }
       if (row_sink().fn) row_sink().fn(row_sink().ctx, jb, end, st);
       mark(st);
       cudaStreamWaitEvent(st, ev_panel, 0);
