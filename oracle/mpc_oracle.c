@@ -227,7 +227,7 @@ void orc_exp_mul(const double *x, const double *y, double *buf, double *out, int
 
 /* _kernels.py:225-255 */
 void orc_exp_div(const double *x, const double *y, double *buf, double *out, int k) {
-    double q[MAX_K + 2], r[MAX_K], t[MAX_K];
+    double q[MAX_K + 2], r[MAX_K] = {0}, t[MAX_K];
     for (int i = 0; i < k; i++) r[i] = x[i];
     int nq = 0;
     for (int it = 0; it < k + 1; it++) {
