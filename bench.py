@@ -321,7 +321,9 @@ def run_b200(args, rank, world):
         hi = torch.empty(im0.shape, dtype=torch.float64, pin_memory=True)
         hp = torch.empty(n, dtype=torch.int64, pin_memory=True)
         times = []
-        for _ in range(max(1, min(args.steps, 1))):
+        # one untimed warm-up call (first-use costs of the staging pool, the
+        # copy stream and the pinned pages), then one timed call
+        for it in range(2):
             hr.numpy()[...] = re0
             hi.numpy()[...] = im0
             torch.cuda.synchronize()
@@ -332,14 +334,16 @@ def run_b200(args, rank, world):
                                  real_kernel=args.real_kernel)
             e1.record(torch.cuda.default_stream(dev))
             torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
+            if it > 0:
+                times.append(e0.elapsed_time(e1))
         t = statistics.median(times)
         # parity spot check of the e2e output against the device result
         same = bool(torch.equal(hp, piv.cpu()))
         e2e = {"value": conv_flops(n) / (t * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(re0.nbytes + im0.nbytes),
                "d2h_bytes_per_step": int(re0.nbytes + im0.nbytes + 8 * n),
-               "ms_per_step": t, "steps": len(times), "pivots_match_device_run": same,
+               "ms_per_step": t, "steps": len(times), "warmup": 1,
+               "pivots_match_device_run": same,
                "api": "paper_2403_16013_b200.lu.factor_inplace (%s, host pointers)"
                       % ("mpc_getrf_ozaki" if ozaki else "mpc_getrf")}
 

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -466,7 +467,11 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
   int64_t e = extent(k, n, n, n, n * n);
   // host factors in pinned memory: finished row blocks stream back while
   // the LU runs (the staged copy-out below then skips them)
-  const bool overlap = sg.host() && n > 0 && is_pinned(re) && is_pinned(im);
+  static const bool overlap_on = [] {  // MPC_HOST_OVERLAP=0: staged copies (A/B)
+    const char* e = getenv("MPC_HOST_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  const bool overlap = overlap_on && sg.host() && n > 0 && is_pinned(re) && is_pinned(im);
   double* dr = sg.map(re, e, !overlap, !overlap);
   double* di = sg.map(im, e, !overlap, !overlap);
   int64_t* dp = sg.map(piv, n, false, true);
