@@ -426,6 +426,21 @@ struct ColH2D {
   }
   void issue(cudaStream_t cs, double* dr, double* di, const double* hr, const double* hi, int k,
              int64_t n, int64_t K, int64_t chunk) {
+    static const bool whole = [] {  // MPC_H2D_WHOLE=1: one 1-D copy per plane (A/B)
+      const char* e = getenv("MPC_H2D_WHOLE");
+      return e && e[0] == '1';
+    }();
+    if (whole) {
+      const size_t bytes = sizeof(double) * (size_t)n * (size_t)n * (size_t)k;
+      ck(cudaMemcpyAsync(dr, hr, bytes, cudaMemcpyHostToDevice, cs), "H2D");
+      ck(cudaMemcpyAsync(di, hi, bytes, cudaMemcpyHostToDevice, cs), "H2D");
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventRecord(e, cs), "cudaEventRecord");
+      lo.push_back(0);
+      ev.push_back(e);
+      return;
+    }
     int64_t c = 0;
     while (c < n) {
       int64_t w = (c < 2 * K) ? K : chunk;
