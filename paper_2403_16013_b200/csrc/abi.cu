@@ -374,97 +374,10 @@ int64_t mpc_lu_panel(int k, int method, int64_t n, double* re, double* im, int64
 }
 
 namespace {
-// pinned (page-locked) host memory: async copies from it do not block the host
-bool is_pinned(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
-// device-to-host copies of finished row blocks on a copy stream (getrf's
-// RowSink), so that the D2H of the factors overlaps the rest of the LU
-struct RowD2H {
-  cudaStream_t cs = nullptr;
-  cudaEvent_t ev = nullptr;
-  const double* dr;
-  const double* di;
-  double* hr;
-  double* hi;
-  int k;
-  int64_t n;
-  static void fn(void* c, int64_t r0, int64_t r1, cudaStream_t st) {
-    auto* s = (RowD2H*)c;
-    ck(cudaEventRecord(s->ev, st), "cudaEventRecord");
-    ck(cudaStreamWaitEvent(s->cs, s->ev, 0), "cudaStreamWaitEvent");
-    const size_t bytes = sizeof(double) * (size_t)(r1 - r0) * (size_t)s->n;
-    for (int q = 0; q < s->k; q++) {
-      const size_t off = (size_t)q * s->n * s->n + (size_t)r0 * s->n;
-      ck(cudaMemcpyAsync(s->hr + off, s->dr + off, bytes, cudaMemcpyDeviceToHost, s->cs), "D2H");
-      ck(cudaMemcpyAsync(s->hi + off, s->di + off, bytes, cudaMemcpyDeviceToHost, s->cs), "D2H");
-    }
-  }
-};
-struct SinkGuard {
-  ~SinkGuard() {
+struct HookGuard {  // getrf's host hooks never outlive the call (exceptions included)
+  ~HookGuard() {
     mpc::row_sink() = mpc::RowSink{nullptr, nullptr};
     mpc::col_source() = mpc::ColSource{nullptr, nullptr, 0};
-  }
-};
-
-// host-to-device copy of the input in column blocks on the copy stream
-// (getrf's ColSource): block boundaries K, 2K, 2K + 4K, ... match the
-// first panel, the narrow update and step 0's update chunks
-struct ColH2D {
-  std::vector<int64_t> lo;  // first column of each block
-  std::vector<cudaEvent_t> ev;
-  size_t waited = 0;
-  ~ColH2D() {
-    for (auto e : ev) cudaEventDestroy(e);
-  }
-  void issue(cudaStream_t cs, double* dr, double* di, const double* hr, const double* hi, int k,
-             int64_t n, int64_t K, int64_t chunk) {
-    static const bool whole = [] {  // MPC_H2D_WHOLE=1: one 1-D copy per plane (A/B)
-      const char* e = getenv("MPC_H2D_WHOLE");
-      return e && e[0] == '1';
-    }();
-    if (whole) {
-      const size_t bytes = sizeof(double) * (size_t)n * (size_t)n * (size_t)k;
-      ck(cudaMemcpyAsync(dr, hr, bytes, cudaMemcpyHostToDevice, cs), "H2D");
-      ck(cudaMemcpyAsync(di, hi, bytes, cudaMemcpyHostToDevice, cs), "H2D");
-      cudaEvent_t e;
-      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-      ck(cudaEventRecord(e, cs), "cudaEventRecord");
-      lo.push_back(0);
-      ev.push_back(e);
-      return;
-    }
-    int64_t c = 0;
-    while (c < n) {
-      int64_t w = (c < 2 * K) ? K : chunk;
-      int64_t c1 = std::min(n, c + w);
-      const size_t pitch = sizeof(double) * (size_t)n;
-      for (int q = 0; q < k; q++) {
-        const size_t off = (size_t)q * n * n + (size_t)c;
-        ck(cudaMemcpy2DAsync(dr + off, pitch, hr + off, pitch, sizeof(double) * (size_t)(c1 - c),
-                             (size_t)n, cudaMemcpyHostToDevice, cs), "H2D");
-        ck(cudaMemcpy2DAsync(di + off, pitch, hi + off, pitch, sizeof(double) * (size_t)(c1 - c),
-                             (size_t)n, cudaMemcpyHostToDevice, cs), "H2D");
-      }
-      cudaEvent_t e;
-      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-      ck(cudaEventRecord(e, cs), "cudaEventRecord");
-      lo.push_back(c);
-      ev.push_back(e);
-      c = c1;
-    }
-  }
-  static void need(void* ctx, int64_t c1, cudaStream_t st) {
-    auto* s = (ColH2D*)ctx;
-    while (s->waited < s->ev.size() && s->lo[s->waited] < c1)
-      ck(cudaStreamWaitEvent(st, s->ev[s->waited++], 0), "cudaStreamWaitEvent");
   }
 };
 }  // namespace
@@ -480,36 +393,19 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
   Stager sg(st);
   if (!sg.classify({re, im, piv})) return MPC_ERR;
   int64_t e = extent(k, n, n, n, n * n);
-  // host factors in pinned memory: finished row blocks stream back while
-  // the LU runs (the staged copy-out below then skips them)
-  static const bool overlap_on = [] {  // MPC_HOST_OVERLAP=0: staged copies (A/B)
-    const char* e = getenv("MPC_HOST_OVERLAP");
-    return !(e && e[0] == '0');
-  }();
-  const bool overlap = overlap_on && sg.host() && n > 0 && is_pinned(re) && is_pinned(im);
+  // host factors in pinned memory: the input arrives in column blocks and
+  // finished row blocks stream back while the LU runs (HostOverlap)
+  const bool overlap = HostOverlap::usable(sg, n, re, im);
   double* dr = sg.map(re, e, !overlap, !overlap);
   double* di = sg.map(im, e, !overlap, !overlap);
   int64_t* dp = sg.map(piv, n, false, true);
   int64_t status = -1;
-  RowD2H d2h;
-  ColH2D h2d;
-  SinkGuard guard;
+  HostOverlap ho;
+  HookGuard guard;
   if (overlap) {
-    ck(cudaStreamCreateWithFlags(&d2h.cs, cudaStreamNonBlocking), "cudaStreamCreate");
-    ck(cudaEventCreateWithFlags(&d2h.ev, cudaEventDisableTiming), "cudaEventCreate");
-    // the copy stream starts after the allocations enqueued on st
-    ck(cudaEventRecord(d2h.ev, st), "cudaEventRecord");
-    ck(cudaStreamWaitEvent(d2h.cs, d2h.ev, 0), "cudaStreamWaitEvent");
-    const int64_t chunk = 4 * K;
-    h2d.issue(d2h.cs, dr, di, re, im, k, n, K, chunk);
-    mpc::col_source() = mpc::ColSource{ColH2D::need, &h2d, chunk};
-    d2h.dr = dr;
-    d2h.di = di;
-    d2h.hr = re;
-    d2h.hi = im;
-    d2h.k = k;
-    d2h.n = n;
-    mpc::row_sink() = mpc::RowSink{RowD2H::fn, &d2h};
+    ho.start(st, dr, di, re, im, k, n, K);
+    mpc::row_sink() = mpc::RowSink{HostOverlap::rows_done, &ho};
+    mpc::col_source() = mpc::ColSource{HostOverlap::need, &ho, ho.chunk};
   }
   if (n > 0) {
     iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dp, n);
@@ -519,17 +415,8 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
     mpc::col_source() = mpc::ColSource{nullptr, nullptr, 0};
     status = w.read_status();
   }
-  if (overlap) {
-    // the staged buffers are freed on st: order it after the copy stream
-    ck(cudaEventRecord(d2h.ev, d2h.cs), "cudaEventRecord");
-    ck(cudaStreamWaitEvent(st, d2h.ev, 0), "cudaStreamWaitEvent");
-  }
+  if (overlap) ho.join(st);
   sg.finish();
-  if (overlap) {
-    ck(cudaStreamSynchronize(d2h.cs), "cudaStreamSynchronize");
-    cudaEventDestroy(d2h.ev);
-    cudaStreamDestroy(d2h.cs);
-  }
   return status;
   MPC_CATCH
 }

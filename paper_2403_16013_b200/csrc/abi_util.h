@@ -2,6 +2,8 @@
 // ozaki.cu): error reporting, pointer classification, host staging, the
 // pivot-reduction workspace.
 #pragma once
+#include <algorithm>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -120,6 +122,113 @@ class Stager {
   cudaStream_t st_;
   bool host_ = false;
   std::vector<Region> regs_;
+};
+
+// pinned (page-locked) host memory: async copies from it do not block the host
+inline bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host-buffer LU (mpc_getrf / mpc_getrf_ozaki on pinned host factors): the
+// input goes host-to-device in column blocks on a copy stream (boundaries
+// K, 2K, then 4K wide -- the first panel, the narrow update and step 0's
+// update chunks), the LU waits per block (need), and each row block is
+// copied back as soon as its step has finished it (rows_done; later steps
+// only touch rows below it).  MPC_HOST_OVERLAP=0 falls back to staged
+// copies; MPC_H2D_WHOLE=1 copies the input as one 1-D block per plane (A/B).
+class HostOverlap {
+ public:
+  int64_t chunk = 0;
+  static bool usable(const Stager& sg, int64_t n, const void* re, const void* im) {
+    static const bool on = [] {
+      const char* e = getenv("MPC_HOST_OVERLAP");
+      return !(e && e[0] == '0');
+    }();
+    return on && sg.host() && n > 0 && is_pinned(re) && is_pinned(im);
+  }
+  void start(cudaStream_t st, double* dr, double* di, double* hr, double* hi, int k, int64_t n,
+             int64_t K) {
+    dr_ = dr;
+    di_ = di;
+    hr_ = hr;
+    hi_ = hi;
+    k_ = k;
+    n_ = n;
+    chunk = 4 * K;
+    ck(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming), "cudaEventCreate");
+    // the copy stream starts after the allocations enqueued on st
+    ck(cudaEventRecord(ev_, st), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(cs_, ev_, 0), "cudaStreamWaitEvent");
+    static const bool whole = [] {
+      const char* e = getenv("MPC_H2D_WHOLE");
+      return e && e[0] == '1';
+    }();
+    const size_t pitch = sizeof(double) * (size_t)n;
+    int64_t c = 0;
+    while (c < n) {
+      int64_t c1 = whole ? n : std::min(n, c + ((c < 2 * K) ? K : chunk));
+      for (int q = 0; q < k; q++) {
+        const size_t off = (size_t)q * n * n + (size_t)c;
+        const size_t w = sizeof(double) * (size_t)(c1 - c);
+        ck(cudaMemcpy2DAsync(dr + off, pitch, hr + off, pitch, w, (size_t)n,
+                             cudaMemcpyHostToDevice, cs_), "H2D");
+        ck(cudaMemcpy2DAsync(di + off, pitch, hi + off, pitch, w, (size_t)n,
+                             cudaMemcpyHostToDevice, cs_), "H2D");
+      }
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventRecord(e, cs_), "cudaEventRecord");
+      lo_.push_back(c);
+      blk_.push_back(e);
+      c = c1;
+    }
+  }
+  // st is about to touch columns [.., c1)
+  static void need(void* ctx, int64_t c1, cudaStream_t st) {
+    auto* s = (HostOverlap*)ctx;
+    while (s->waited_ < s->blk_.size() && s->lo_[s->waited_] < c1)
+      ck(cudaStreamWaitEvent(st, s->blk_[s->waited_++], 0), "cudaStreamWaitEvent");
+  }
+  // rows [r0, r1) are final once the work enqueued on st so far completes
+  static void rows_done(void* ctx, int64_t r0, int64_t r1, cudaStream_t st) {
+    auto* s = (HostOverlap*)ctx;
+    ck(cudaEventRecord(s->ev_, st), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(s->cs_, s->ev_, 0), "cudaStreamWaitEvent");
+    const size_t bytes = sizeof(double) * (size_t)(r1 - r0) * (size_t)s->n_;
+    for (int q = 0; q < s->k_; q++) {
+      const size_t off = (size_t)q * s->n_ * s->n_ + (size_t)r0 * s->n_;
+      ck(cudaMemcpyAsync(s->hr_ + off, s->dr_ + off, bytes, cudaMemcpyDeviceToHost, s->cs_), "D2H");
+      ck(cudaMemcpyAsync(s->hi_ + off, s->di_ + off, bytes, cudaMemcpyDeviceToHost, s->cs_), "D2H");
+    }
+  }
+  // order st (the staged buffers are freed on it) after the copy stream
+  void join(cudaStream_t st) {
+    ck(cudaEventRecord(ev_, cs_), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(st, ev_, 0), "cudaStreamWaitEvent");
+  }
+  ~HostOverlap() {
+    if (!cs_) return;
+    cudaStreamSynchronize(cs_);
+    for (auto e : blk_) cudaEventDestroy(e);
+    cudaEventDestroy(ev_);
+    cudaStreamDestroy(cs_);
+  }
+
+ private:
+  cudaStream_t cs_ = nullptr;
+  cudaEvent_t ev_ = nullptr;
+  double *dr_ = nullptr, *di_ = nullptr, *hr_ = nullptr, *hi_ = nullptr;
+  int k_ = 0;
+  int64_t n_ = 0;
+  std::vector<int64_t> lo_;
+  std::vector<cudaEvent_t> blk_;
+  size_t waited_ = 0;
 };
 
 // pivot-reduction workspace + status word, stream ordered

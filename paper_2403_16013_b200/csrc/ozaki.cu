@@ -467,10 +467,20 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
   Stager sg(st);
   if (!sg.classify({re, im, piv})) return MPC_ERR;
   int64_t e = extent(k, n, n, n, n * n);
-  double* dr = sg.map(re, e, true, true);
-  double* di = sg.map(im, e, true, true);
+  // pinned host factors: copies overlapped with the LU as in mpc_getrf
+  const bool overlap = HostOverlap::usable(sg, n, re, im);
+  double* dr = sg.map(re, e, !overlap, !overlap);
+  double* di = sg.map(im, e, !overlap, !overlap);
   int64_t* dp = sg.map(piv, n, true, true);
   int64_t status = -1;
+  HostOverlap ho;
+  if (overlap) ho.start(st, dr, di, re, im, k, n, K);
+  auto need = [&](int64_t c1) {
+    if (overlap) HostOverlap::need(&ho, std::min(c1, n), st);
+  };
+  auto rows_done = [&](int64_t r0, int64_t r1) {
+    if (overlap) HostOverlap::rows_done(&ho, r0, r1, st);
+  };
   if (n > 0) {
     const mpc::OpsTable* T = table_for(k);
     bool use3m = method == 3;
@@ -512,14 +522,19 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
       tev.push_back(e);
     };
     mark(st);
+    need(std::min(K, n));
     T->panel_rec(use3m, A, n, 0, std::min(K, n), dp, w.ws, st);
     mark(st);
     for (int64_t jb = 0; jb < n; jb += K) {
       int64_t kw = std::min(K, n - jb);
       int64_t end = jb + kw;
       T->laswp(A, 0, jb, dp, jb, end, st, w.ws.status);  // left of the panel
-      if (end == n) break;
+      if (end == n) {
+        rows_done(jb, end);
+        break;
+      }
       int64_t kw2 = std::min(K, n - end);
+      if (jb == 0) need(end + kw2);
       update_cols(jb, kw, end, end + kw2, st);
       cudaEventRecord(ev_narrow, st);
       mark(st);
@@ -527,7 +542,17 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
       T->panel_rec(use3m, A, n, end, kw2, dp, w.ws, sp);
       cudaEventRecord(ev_panel, sp);
       mark(sp);
-      update_cols(jb, kw, end + kw2, n, st);
+      if (jb == 0 && overlap) {
+        // step 0 in column chunks behind their host-to-device blocks (the
+        // Ozaki update is per column range, so no bits change)
+        for (int64_t c0 = end + kw2; c0 < n; c0 += ho.chunk) {
+          need(c0 + ho.chunk);
+          update_cols(jb, kw, c0, std::min(n, c0 + ho.chunk), st);
+        }
+      } else {
+        update_cols(jb, kw, end + kw2, n, st);
+      }
+      rows_done(jb, end);
       mark(st);
       cudaStreamWaitEvent(st, ev_panel, 0);
       mark(st);
@@ -555,6 +580,7 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
     cudaStreamDestroy(sp);
     status = w.read_status();
   }
+  if (overlap) ho.join(st);
   sg.finish();
   return status;
   MPC_CATCH

@@ -231,3 +231,28 @@ def test_factor_inplace_pinned_overlap(mp, k, n, K):
     assert np.array_equal(pp, gp) and np.array_equal(pp, dp.cpu().numpy())
     assert pr.numpy().tobytes() == gr.tobytes() == dr.cpu().numpy().tobytes()
     assert pi.numpy().tobytes() == gi.tobytes() == di.cpu().numpy().tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,K", [(300, 64), (96, 96)])
+def test_factor_inplace_pinned_overlap_ozaki(mp, n, K):
+    """The Ozaki LU on pinned host factors (overlapped copies, chunked step-0
+    update) equals its device path bit for bit."""
+    import torch
+
+    from paper_2403_16013_b200 import lu as lum, problems
+
+    re, im = problems.lu_matrix(n, 2, 11)
+    pr = torch.empty(re.shape, dtype=torch.float64, pin_memory=True)
+    pi = torch.empty(im.shape, dtype=torch.float64, pin_memory=True)
+    pr.numpy()[...] = re
+    pi.numpy()[...] = im
+    pp = lum.factor_inplace(pr.numpy(), pi.numpy(), K, real_kernel="ozaki")
+    dev = torch.device("cuda", 0)
+    dr, di = torch.from_numpy(re).to(dev), torch.from_numpy(im).to(dev)
+    dp = torch.empty(n, dtype=torch.int64, device=dev)
+    lum.factor_inplace(dr, di, K, piv=dp, real_kernel="ozaki")
+    torch.cuda.synchronize()
+    assert np.array_equal(pp, dp.cpu().numpy())
+    assert pr.numpy().tobytes() == dr.cpu().numpy().tobytes()
+    assert pi.numpy().tobytes() == di.cpu().numpy().tobytes()
