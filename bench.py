@@ -61,7 +61,60 @@ def parse():
     p.add_argument("--no-alt", action="store_true",
                    help="skip the secondary measurement with the other real kernel")
     p.add_argument("--cpu-n", type=int, default=CPU_SAMPLE_N)
+    p.add_argument("--dry-run", action="store_true",
+                   help="N-rank launch plumbing only (gloo on CPU, no LU): checks that "
+                        "--gpus N really starts N ranks and reports n_gpus = N")
     return p.parse_args()
+
+
+def free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn(args):
+    """--gpus N > 1 outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1 and relay their output; fails loudly
+    when fewer than N GPUs are visible (unless --dry-run / --impl reference,
+    which need none)."""
+    if not args.dry_run and args.impl == "b200":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) "
+                             "are visible\n")
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.join(ROOT, "bench.py")] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
+
+
+def run_dry(args, rank, world):
+    """The N-rank plumbing of the bench without a GPU: gloo process group,
+    barrier, a per-rank 'step time' reduced with MAX, rank 0 prints one JSON
+    line.  No measurement (value null)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    dist.barrier()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ranks = [None] * world
+    dist.all_gather_object(ranks, {"rank": rank, "pid": os.getpid(),
+                                   "local_rank": int(os.environ.get("LOCAL_RANK", 0))})
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "GFLOP/s", "n_gpus": world,
+                          "dry_run": True, "ranks": ranks, "max_over_ranks": float(t.item()),
+                          "config": {"workload": workload(args)}}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def conv_flops(n):
@@ -413,7 +466,7 @@ def run_b200(args, rank, world):
                                               seed=args.seed)
 
     out = {
-        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64 (double-double expansion)",
         "data": "synthetic (seeded Philox U(-1,1), SURVEY.md 8d)",
@@ -513,8 +566,12 @@ def main():
         args.n = 1024 if args.workload == "gemm" else 16384
     if args.workload == "gemm" and args.impl == "b200":
         return run_gemm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.dry_run:
+        return run_dry(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_b200(args, rank, world)

@@ -119,11 +119,35 @@ int mpc_laswp(int k, int64_t ncols, double* re, double* im, int64_t ld, int64_t 
 int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* im,
                   int64_t* piv, void* stream);
 
+/* Multi-GPU lu._factor (mpc_getrf with ngpus and
+ * lookahead): 1-D block-column-cyclic over `ngpus` devices of this process
+ * (device ordinals current, current+1, ...), panel + pivots + status pulled
+ * by every rank from the panel owner over NVLink peer copies, depth-1
+ * lookahead when lookahead != 0.  real_kernel 0 = the EFT GEMM (mpc_getrf),
+ * 1 = the Ozaki tensor-core GEMM (mpc_getrf_ozaki; d, split_bits as there).
+ * Pointers: host (pageable or pinned) or device memory; piv receives the
+ * pivots.  Bit-identical to mpc_getrf / mpc_getrf_ozaki.  ngpus = 1 is
+ * mpc_getrf (or mpc_getrf_ozaki); ngpus above the device count is an error
+ * unless MPC_MGPU_OVERSUBSCRIBE=1 (ranks share devices; test mode).
+ * Synchronous (returns the status like mpc_getrf). */
+int64_t mpc_getrf_ngpu(int k, int method, int64_t n, int64_t K, double* re, double* im,
+                       int64_t* piv, int ngpus, int lookahead, int real_kernel, int d,
+                       int split_bits, void* stream);
+
 /* solve_fb (_kernels.py:708-775) behind solve (lu.py:205-218): x from
  * L U x = P b on packed factors; b (k x n planes, Re and Im) is overwritten.
  * The caller checks the U diagonal for exact zeros (lu.py:213-215). */
 int mpc_getrs(int k, int method, int64_t n, const double* re, const double* im,
               const int64_t* piv, double* b_re, double* b_im, void* stream);
+
+/* The halves of solve_fb (_kernels.py:708-775) separately (LAPACK getrs
+ * style): phases 1 = the interchanges (_kernels.py:711-721) + the unit-lower
+ * forward substitution (734-752; bit-identical to the reference), 2 = the
+ * backward substitution with the cdiv by U_ii (753-775; b holds the forward
+ * result), 3 = both (= mpc_getrs). */
+int mpc_getrs_phases(int k, int method, int64_t n, const double* re, const double* im,
+                     const int64_t* piv, double* b_re, double* b_im, int phases,
+                     void* stream);
 
 /* ---- Ozaki scheme (ozaki.py:79-159): the alternative real kernel ---- */
 /* ozaki_split (ozaki.py:79-108) of a (rows x cols) planar operand into d
@@ -160,7 +184,7 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
  * `mask` (bit c = class c below; 0 disables).  Clears previous records. */
 void mpc_prof_enable(int mask);
 /* Sum per kernel class (0 GEMM, 1 S-update, 2 panel, 3 TRSM diagonal,
- * 4 LASWP, 5 other) of event-timed ms, algorithmic FP64 ops (op model v1)
+ * 4 LASWP, 5 other, 6 solve) of event-timed ms, algorithmic FP64 ops (op model v1)
  * and launch counts since the last mpc_prof_enable(1).  Returns the number of
  * classes or MPC_ERR. */
 int mpc_prof_summary(double* ms, double* ops, long long* count, int nclass);

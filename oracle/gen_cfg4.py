@@ -1,0 +1,96 @@
+"""Golden digests for BASELINE config 4 (n=16384, K=512, DD, 3M), both inputs.
+
+TEST INFRASTRUCTURE ONLY.  The unmodified reference needs about 5 h and
+~48 GiB per input at 8 cores for this size, so the
+factorization is run by the CPU oracle (oracle/mpc_oracle.c, OpenMP), which
+is pinned bit for bit to the reference's own outputs at configs 0-3 and to
+the ill-conditioned input at n=4096 (tests/test_oracle_golden.py,
+tests/golden/cfg*.json, tests/golden/ill_n4096.json).  It restates
+lu._factor (lu.py:129-163), _pivot_row (_kernels.py:568-594) and solve_fb
+(_kernels.py:708-775).
+
+Writes tests/golden/cfg4.json: per input the pivots, SHA-256 of the packed
+factor planes (all planes together and one per limb plane), the right-hand
+side digest and the oracle solve's x digest and forward error.
+
+    python oracle/gen_cfg4.py [uniform] [ill]      # ~1-2 h each at 8 cores
+"""
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from oracle import oracle  # noqa: E402
+from paper_2403_16013_b200 import problems  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+N, K, k = 16384, 512, 2
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def fwd_err(xr, xi):
+    """max_i |x_i - (1+1i)| / max |x_true| in binary64 from the limb-wise
+    difference (x_true = 1 + 1i, |x_true| = sqrt 2)."""
+    dr = (xr[0] - 1.0) + xr[1:].sum(axis=0)
+    di = (xi[0] - 1.0) + xi[1:].sum(axis=0)
+    return float(np.max(np.hypot(dr, di)) / np.sqrt(2.0))
+
+
+def run(variant):
+    ill = variant == "ill"
+    re, im = problems.lu_matrix(N, k, 1, ill_conditioned=ill)
+    rec = {"variant": variant, "n": N, "K": K, "k": k, "method": "3m", "seed": 1,
+           "input_digest": digest(re, im)}
+    xr, xi = problems.x_true(N, k)
+    br, bi = oracle.cgemm(re, im, xr.reshape(k, N, 1), xi.reshape(k, N, 1), "4m")
+    br, bi = br[:, :, 0].copy(), bi[:, :, 0].copy()
+    rec["b_digest"] = digest(np.array([br, bi]))
+    t0 = time.perf_counter()
+    fr, fi, piv, st = oracle.factor(re, im, K, "3m")
+    rec["seconds"] = time.perf_counter() - t0
+    rec["threads"] = os.cpu_count()
+    rec["status"] = st
+    del re, im
+    rec["pivots"] = [int(p) for p in piv]
+    rec["digest"] = digest(fr, fi)
+    rec["digest_planes"] = [digest(fr[c]) for c in range(k)] + [digest(fi[c]) for c in range(k)]
+    t0 = time.perf_counter()
+    x_r, x_i = oracle.solve_fb(fr, fi, piv, br, bi, "3m")
+    rec["solve_seconds"] = time.perf_counter() - t0
+    rec["x_digest"] = digest(x_r, x_i)
+    rec["fwd_err"] = fwd_err(x_r, x_i)
+    print(variant, rec["seconds"], rec["fwd_err"], flush=True)
+    return rec
+
+
+def main(variants):
+    path = os.path.join(GOLD, "cfg4.json")
+    res = {"generator": "oracle/gen_cfg4.py (CPU oracle, pinned to the reference)",
+           "cases": []}
+    if os.path.exists(path):
+        res = json.load(open(path))
+    done = {c["variant"] for c in res["cases"]}
+    for v in variants:
+        if v in done:
+            continue
+        res["cases"].append(run(v))
+        with open(path, "w") as fh:
+            json.dump(res, fh)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["uniform", "ill"])

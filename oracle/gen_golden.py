@@ -11,6 +11,7 @@ need is committed as these files.
     python oracle/gen_golden.py cfg0 cfg1    # BASELINE configs 0 and 1 (digests)
     python oracle/gen_golden.py cfg2         # config 2, n=4096 DD LU (~3 min)
     python oracle/gen_golden.py cfg3         # config 3, TD/QD n=2048 LU (long)
+    python oracle/gen_golden.py cfg2_4m ill  # config 2 in 4M; ill-conditioned n=4096
 """
 
 import hashlib
@@ -322,6 +323,43 @@ def gen_cfg2():
         json.dump(res, fh)
 
 
+def gen_cfg2_4m():
+    """Adds the 4M factorization of the config-2 input to cfg2.json."""
+    path = os.path.join(GOLD, "cfg2.json")
+    res = json.load(open(path))
+    if any(c["method"] == "4m" for c in res["cases"]):
+        return
+    n, k, K = 4096, 2, 256
+    re, im = problems.lu_matrix(n, k, 1)
+    assert digest(re, im) == res["input_digest"]
+    b = rhs(re, im)
+    rec, f = _lu_record(re, im, K, "4m", b)
+    rec.update(seed=1, n=n, k=k, b_digest=digest(b))
+    res["cases"].append(rec)
+    print("cfg2 4m", rec["seconds"], rec.get("solve_seconds"))
+    with open(path, "w") as fh:
+        json.dump(res, fh)
+
+
+def gen_ill(n=4096, K=256):
+    """Config 4's ill-conditioned input (row i scaled by 10^(-12 i/n)) at a
+    size the reference factors in minutes: pivots, plane digests, solve."""
+    res = {"meta": meta(), "cases": []}
+    k = 2
+    re, im = problems.lu_matrix(n, k, 1, ill_conditioned=True)
+    res["input_digest"] = digest(re, im)
+    b = rhs(re, im)
+    for meth in ("3m",):
+        rec, f = _lu_record(re, im, K, meth, b)
+        rec.update(seed=1, n=n, k=k, b_digest=digest(b), ill_conditioned=True)
+        rec["digest_planes"] = [digest(f.packed.re_plane.data[c]) for c in range(k)] + \
+            [digest(f.packed.im_plane.data[c]) for c in range(k)]
+        res["cases"].append(rec)
+        print("ill", n, meth, rec["seconds"], rec.get("solve_seconds"), flush=True)
+    with open(os.path.join(GOLD, f"ill_n{n}.json"), "w") as fh:
+        json.dump(res, fh)
+
+
 def gen_cfg3(n=2048, K=128):
     path = os.path.join(GOLD, f"cfg3_n{n}.json")
     res = {"meta": meta(), "cases": []}
@@ -392,4 +430,5 @@ if __name__ == "__main__":
             gen_cfg3(n=512, K=128)
             continue
         {"small": gen_small, "cfg0": gen_cfg0, "cfg1": gen_cfg1, "cfg2": gen_cfg2,
-         "cfg3": gen_cfg3, "ozaki": gen_ozaki}[what]()
+         "cfg3": gen_cfg3, "ozaki": gen_ozaki, "cfg2_4m": gen_cfg2_4m,
+         "ill": gen_ill}[what]()

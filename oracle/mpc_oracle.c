@@ -582,10 +582,12 @@ int64_t orc_factor(int k, int use3m, int64_t n, int64_t K, double *re, double *i
 }
 
 /* solve_fb, _kernels.py:708-775 (b overwritten by x; vectors (k, n)) */
-void orc_solve_fb(int k, int use3m, int64_t n, const double *re, const double *im,
-                  const int64_t *piv, double *br, double *bi) {
+/* phases: 1 = interchanges + forward sweep, 2 = backward sweep, 3 = both
+ * (solve_fb itself) -- the halves checked separately by the GPU tests. */
+void orc_solve_phases(int k, int use3m, int64_t n, const double *re, const double *im,
+                      const int64_t *piv, double *br, double *bi, int phases) {
     int64_t ps = n * n;
-    for (int64_t i = 0; i < n; i++) {
+    for (int64_t i = 0; (phases & 1) && i < n; i++) {
         int64_t p = piv[i];
         if (p != i) {
             for (int c = 0; c < k; c++) {
@@ -600,7 +602,7 @@ void orc_solve_fb(int k, int use3m, int64_t n, const double *re, const double *i
     }
     double xr[MAX_K], xi[MAX_K], yr[MAX_K], yi[MAX_K], lr[MAX_K], li[MAX_K];
     double pr[MAX_K], pi[MAX_K], buf[SCRATCH_MAX];
-    for (int64_t i = 1; i < n; i++) {
+    for (int64_t i = 1; (phases & 1) && i < n; i++) {
         for (int c = 0; c < k; c++) {
             xr[c] = br[c * n + i];
             xi[c] = bi[c * n + i];
@@ -621,7 +623,7 @@ void orc_solve_fb(int k, int use3m, int64_t n, const double *re, const double *i
             bi[c * n + i] = xi[c];
         }
     }
-    for (int64_t i = n - 1; i >= 0; i--) {
+    for (int64_t i = n - 1; (phases & 2) && i >= 0; i--) {
         for (int c = 0; c < k; c++) {
             xr[c] = br[c * n + i];
             xi[c] = bi[c * n + i];
@@ -647,6 +649,11 @@ void orc_solve_fb(int k, int use3m, int64_t n, const double *re, const double *i
             bi[c * n + i] = yi[c];
         }
     }
+}
+
+void orc_solve_fb(int k, int use3m, int64_t n, const double *re, const double *im,
+                  const int64_t *piv, double *br, double *bi) {
+    orc_solve_phases(k, use3m, n, re, im, piv, br, bi, 3);
 }
 
 /* ------------------------------------------------------- scalar wrappers */

@@ -67,6 +67,7 @@ def _load():
                                     _i64, _i64]),
         "orc_factor": (_i64, [_int, _int, _i64, _i64, _dp, _dp, _i64p]),
         "orc_solve_fb": (None, [_int, _int, _i64, _dp, _dp, _i64p, _dp, _dp]),
+        "orc_solve_phases": (None, [_int, _int, _i64, _dp, _dp, _i64p, _dp, _dp, _int]),
         "orc_set_threads": (_int, [_int]),
     }
     for name, (res, args) in sig.items():
@@ -253,12 +254,13 @@ def factor(re, im, K, method="3m"):
     return re, im, piv, int(st)
 
 
-def solve_fb(re, im, piv, br, bi, method="3m"):
-    """solve_fb, _kernels.py:708-775 -> (xr, xi)"""
+def solve_fb(re, im, piv, br, bi, method="3m", phases=3):
+    """solve_fb, _kernels.py:708-775 -> (xr, xi); phases 1 = interchanges +
+    forward sweep only, 2 = backward sweep only, 3 = both"""
     re, im = _c(re), _c(im)
     k, n, _ = re.shape
     xr, xi = _c(br).copy(), _c(bi).copy()
     piv = np.ascontiguousarray(piv, dtype=np.int64)
-    _load().orc_solve_fb(k, int(method == "3m"), n, _d(re), _d(im),
-                         piv.ctypes.data_as(_i64p), _d(xr), _d(xi))
+    _load().orc_solve_phases(k, int(method == "3m"), n, _d(re), _d(im),
+                             piv.ctypes.data_as(_i64p), _d(xr), _d(xi), int(phases))
     return xr, xi

@@ -33,6 +33,8 @@ _SIGS = {
     "mpc_laswp": (_i, [_i, _i64, _p, _p, _i64, _i64, _p, _i64, _i64, _p]),
     "mpc_getrf": (_i64, [_i, _i, _i64, _i64, _p, _p, _p, _p]),
     "mpc_getrs": (_i, [_i, _i, _i64, _p, _p, _p, _p, _p, _p]),
+    "mpc_getrf_ngpu": (ctypes.c_int64, [_i, _i, _i64, _i64, _p, _p, _p, _i, _i, _i, _i, _i, _p]),
+    "mpc_getrs_phases": (_i, [_i, _i, _i64, _p, _p, _p, _p, _p, _i, _p]),
     "mpc_ozaki_split": (_i, [_i, _i64, _i64, _p, _i64, _i64, _i, _i, _i, _p, _p, _p]),
     "mpc_acc_plane": (_i, [_i, _i64, _i64, _p, _i64, _i64, _p, _i64, _p]),
     "mpc_f64_gemm": (_i, [_i64, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, _p]),
@@ -48,7 +50,7 @@ _SIGS = {
     "mpc_int8_peak": (_d, [_i, _p]),
 }
 
-PROF_CLASSES = ("gemm", "supdate", "panel", "trsm_diag", "laswp", "other")
+PROF_CLASSES = ("gemm", "supdate", "panel", "trsm_diag", "laswp", "other", "solve")
 
 MPC_ERR = -2
 

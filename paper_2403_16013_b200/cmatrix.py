@@ -105,6 +105,10 @@ class KernelChoice:
     d: Optional[int] = None
     split_bits: Optional[int] = None
     threads: int = 1
+    # B200 addition: GPUs of this process the LU is
+    # distributed over (1-D block-column-cyclic, mpc_getrf_ngpu); never
+    # changes any bit of the result
+    ngpus: int = 1
 
     def validate(self):
         if self.method not in METHODS:
@@ -119,6 +123,8 @@ class KernelChoice:
             raise ValueError("d must be >= 1")
         if self.threads < 1:
             raise ValueError("threads must be >= 1")
+        if self.ngpus < 1:
+            raise ValueError("ngpus must be >= 1")
         return self
 
     def with_threads(self, threads):

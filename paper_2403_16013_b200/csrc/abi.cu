@@ -423,6 +423,12 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
 
 int mpc_getrs(int k, int method, int64_t n, const double* re, const double* im,
               const int64_t* piv, double* b_re, double* b_im, void* stream) {
+  return mpc_getrs_phases(k, method, n, re, im, piv, b_re, b_im, 3, stream);
+}
+
+int mpc_getrs_phases(int k, int method, int64_t n, const double* re, const double* im,
+                     const int64_t* piv, double* b_re, double* b_im, int phases, void* stream) {
+  if (phases < 1 || phases > 3) return fail("phases must be 1, 2 or 3");
   if (bad_k(k)) return fail("k must be 2, 3 or 4");
   if (bad_method(method)) return fail("method must be 3 (3M) or 4 (4M)");
   if (n < 0) return fail("negative dimension");
@@ -437,7 +443,7 @@ int mpc_getrs(int k, int method, int64_t n, const double* re, const double* im,
   double* dbr = sg.map(b_re, (int64_t)k * n, true, true);
   double* dbi = sg.map(b_im, (int64_t)k * n, true, true);
   if (n > 0)
-    table_for(k)->getrs(method == 3, mpc::View{dr, di, n, n * n}, n, dp, dbr, dbi, st);
+    table_for(k)->getrs(method == 3, mpc::View{dr, di, n, n * n}, n, dp, dbr, dbi, phases, st);
   sg.finish();
   return 0;
   MPC_CATCH

@@ -817,99 +817,211 @@ __global__ void trsm_diag_kernel(View L, View X, int64_t kb, int64_t M, int use3
 }
 
 // -------------------------------------------------------------- solve
-// solve_fb's interchanges (_kernels.py:711-721): one thread per limb plane
+// solve_fb (_kernels.py:708-775) as a blocked triangular solve with
+// KB-row diagonal blocks, one launch per block and direction.
+//
+// Interchanges: the reference swaps b_i <-> b_{piv[i]} for i ascending
+// (_kernels.py:711-721).  The same swaps applied to an index vector (one
+// thread, shared memory) give idx with b_new[i] = b_old[idx[i]]; a parallel
+// gather then permutes all 2k limb planes at once.
 template <int K>
-__global__ void vec_swap_kernel(double* br, double* bi, int64_t n, const int64_t* piv) {
-  int q = threadIdx.x;
-  if (q >= 2 * K) return;
-  double* b = (q < K) ? br + q * n : bi + (q - K) * n;
-  for (int64_t i = 0; i < n; i++) {
-    int64_t p = piv[i];
-    if (p != i) {
-      double x = b[i];
-      b[i] = b[p];
-      b[p] = x;
-    }
+__global__ void perm_compose_kernel(const int64_t* __restrict__ piv, int64_t n,
+                                    int64_t* __restrict__ idx, int use_smem) {
+  extern __shared__ int sidx[];
+  if (use_smem) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sidx[i] = (int)i;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int64_t i = 0; i < n; i++) {
+        int64_t p = __ldg(piv + i);
+        if (p != i) {
+          int x = sidx[i];
+          sidx[i] = sidx[p];
+          sidx[p] = x;
+        }
+      }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) idx[i] = sidx[i];
+  } else {  // n beyond shared memory: the same sequence on the global vector
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) idx[i] = i;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int64_t i = 0; i < n; i++) {
+        int64_t p = __ldg(piv + i);
+        if (p != i) {
+          int64_t x = idx[i];
+          idx[i] = idx[p];
+          idx[p] = x;
+        }
+      }
   }
 }
 
-// Forward substitution, block-diagonal part: rows [r0, r0+kb) in order,
-// x_i -= cmul(L_ij, x_j), j ascending (_kernels.py:734-752).  Single thread.
+// y[q][i] = b_q[idx[i]] for the 2k limb planes (q < k: Re, else Im)
 template <int K>
-__global__ void fwd_diag_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
-                                int64_t kb, int use3m) {
-  for (int64_t i = r0 + 1; i < r0 + kb; i++) {
-    Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
-    for (int64_t j = r0; j < i; j++) {
-      Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
-      Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
-      Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
-      xr = exp_sub(xr, p.re);
-      xi = exp_sub(xi, p.im);
-    }
-    stexp_<K>(br + i, n, xr);
-    stexp_<K>(bi + i, n, xi);
+__global__ void perm_gather_kernel(const double* br, const double* bi, const int64_t* idx,
+                                   int64_t n, double* y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 2 * K * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int q = (int)(e / n);
+    int64_t i = e - (int64_t)q * n;
+    int64_t s = idx[i];
+    y[e] = q < K ? br[q * n + s] : bi[(q - K) * n + s];
   }
 }
 
-// Forward substitution, off-diagonal part: rows i >= r0+kb subtract the
-// block's contributions j in [r0, r0+kb) ascending (same per-element order
-// as the reference's row-oriented loop).
 template <int K>
-__global__ void fwd_update_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
-                                  int64_t kb, int use3m) {
-  int64_t i = r0 + kb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
-  for (int64_t j = r0; j < r0 + kb; j++) {
-    Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
-    Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
-    Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+struct SolveCfg {
+  static constexpr int KB = 32;                // diagonal block = one warp
+  static constexpr int RT = K == 2 ? 128 : 64;  // off-diagonal rows per CTA (one per thread)
+  static constexpr int LDS = KB + 1;            // padded row: conflict-free 8-byte reads
+  static constexpr size_t SMEM = sizeof(double) * 2 * K * (size_t)(KB + RT) * LDS;
+};
+
+// One diagonal block [r0, r0+kb) of the forward (FWD: unit lower, reference
+// order) or backward (upper, cdiv by U_ii) substitution, plus the
+// off-diagonal update of RT rows per CTA (FWD: rows >= r0+kb, else rows
+// < r0).  Working values live in (wr, wi) -- (2k, n)-shaped planar vectors
+// (limb c of entry i at c*n + i) -- and the block's final values go to
+// (fr, fi), so no CTA overwrites what another still reads.
+//   * diagonal block (every CTA, redundantly, in warp 0): lane r holds x_r;
+//     FWD: for s ascending, x_s is final, broadcast by shuffle, lanes r > s
+//     apply x_r -= cmul(L_rs, x_s) -- exactly the reference's chain order
+//     (j ascending); BWD: for s descending, lane s divides by U_ss, then
+//     lanes r < s apply x_r -= cmul(U_rs, x_s).
+//   * off-diagonal rows: one thread per row, x_i -= cmul(F_ij, x_j) for j
+//     ascending over the block, F tile staged coalesced in shared memory.
+// Forward chains therefore equal the reference's (blocks ascending, j
+// ascending within each): bitwise.  Backward applies blocks in descending
+// order -- the reference's row chain (j ascending up to n) is inherently
+// sequential (n^2/2 dependent steps) -- so it is tolerance-parity.
+template <int K, bool FWD>
+__global__ void __launch_bounds__(SolveCfg<K>::RT)
+    trsv_block_kernel(View F, double* wr, double* wi, double* fr, double* fi, int64_t n,
+                      int64_t r0, int64_t kb, int use3m) {
+  using C = SolveCfg<K>;
+  constexpr int KB = C::KB, RT = C::RT, LDS = C::LDS;
+  extern __shared__ double sm[];
+  double* Ld = sm;                      // [2k][KB][LDS] diagonal block
+  double* Lt = sm + 2 * K * KB * LDS;   // [2k][RT][LDS] off-diagonal rows
+  __shared__ double xs[2 * K][KB];      // the block's final x
+  __shared__ double xsum[K][KB];        // Re + Im of x (3M operand sums)
+  const int t = threadIdx.x;
+  const int64_t row0 = FWD ? r0 + kb + (int64_t)blockIdx.x * RT : (int64_t)blockIdx.x * RT;
+  const int64_t rowEnd = FWD ? n : r0;
+  // staging with cp.async (no register round trip, every load in flight at
+  // once): group 0 = the diagonal block, group 1 = the off-diagonal rows,
+  // which keep landing while warp 0 solves the diagonal block
+  for (int e = t; e < 2 * K * KB * KB; e += RT) {
+    int q = e / (KB * KB), rr = (e / KB) % KB, jj = e % KB;
+    const double* base = q < K ? F.re + q * F.ps : F.im + (q - K) * F.ps;
+    bool ok = rr < kb && jj < kb;
+    cp_async8(&Ld[(q * KB + rr) * LDS + jj], ok ? base + (r0 + rr) * F.ld + r0 + jj : base, ok);
+  }
+  cp_async_commit();
+  for (int e = t; e < 2 * K * RT * KB; e += RT) {
+    int q = e / (RT * KB), rr = (e / KB) % RT, jj = e % KB;
+    int64_t i = row0 + rr;
+    const double* base = q < K ? F.re + q * F.ps : F.im + (q - K) * F.ps;
+    bool ok = i < rowEnd && jj < kb;
+    cp_async8(&Lt[(q * RT + rr) * LDS + jj], ok ? base + i * F.ld + r0 + jj : base, ok);
+  }
+  cp_async_commit();
+  cp_async_wait<1>();
+  __syncthreads();
+  if (t < 32) {
+    const int r = t;
+    const bool live = r < kb;
+    Exp<K> xr = exp_zero<K>(), xi = exp_zero<K>();
+    if (live) {
+      xr = ldexp_<K>(wr + r0 + r, n);
+      xi = ldexp_<K>(wi + r0 + r, n);
+    }
+    auto ld_d = [&](int rr, int jj, Exp<K>& lr, Exp<K>& li) {
+#pragma unroll
+      for (int c = 0; c < K; c++) {
+        lr.c[c] = Ld[(c * KB + rr) * LDS + jj];
+        li.c[c] = Ld[((K + c) * KB + rr) * LDS + jj];
+      }
+    };
+    if constexpr (FWD) {
+      for (int s = 0; s + 1 < (int)kb; s++) {
+        Exp<K> yr, yi;
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+          yr.c[c] = __shfl_sync(0xffffffffu, xr.c[c], s);
+          yi.c[c] = __shfl_sync(0xffffffffu, xi.c[c], s);
+        }
+        if (live && r > s) {
+          Exp<K> lr, li;
+          ld_d(r, s, lr, li);
+          Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+          xr = exp_sub(xr, p.re);
+          xi = exp_sub(xi, p.im);
+        }
+      }
+    } else {
+      for (int s = (int)kb - 1; s >= 0; s--) {
+        if (r == s) {
+          Exp<K> ur, ui;
+          ld_d(s, s, ur, ui);
+          Cx<K> q = cdiv(xr, xi, ur, ui);
+          xr = q.re;
+          xi = q.im;
+        }
+        Exp<K> yr, yi;
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+          yr.c[c] = __shfl_sync(0xffffffffu, xr.c[c], s);
+          yi.c[c] = __shfl_sync(0xffffffffu, xi.c[c], s);
+        }
+        if (r < s) {
+          Exp<K> lr, li;
+          ld_d(r, s, lr, li);
+          Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
+          xr = exp_sub(xr, p.re);
+          xi = exp_sub(xi, p.im);
+        }
+      }
+    }
+    if (live) {
+      Exp<K> sx = exp_add(xr, xi);  // cmul_3m_core's b-operand sum (_kernels.py:534)
+#pragma unroll
+      for (int c = 0; c < K; c++) {
+        xs[c][r] = xr.c[c];
+        xs[K + c][r] = xi.c[c];
+        xsum[c][r] = sx.c[c];
+      }
+      if (blockIdx.x == 0) {
+        stexp_<K>(fr + r0 + r, n, xr);
+        stexp_<K>(fi + r0 + r, n, xi);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  const int64_t i = row0 + t;
+  if (i >= rowEnd) return;
+  Exp<K> xr = ldexp_<K>(wr + i, n), xi = ldexp_<K>(wi + i, n);
+  // x_i -= cmul(F_ij, x_j), j ascending; the products do not depend on x_i,
+  // so unrolling lets the next products overlap the subtraction chain
+#pragma unroll 4
+  for (int j = 0; j < (int)kb; j++) {
+    Exp<K> lr, li, yr, yi, sy;
+#pragma unroll
+    for (int c = 0; c < K; c++) {
+      lr.c[c] = Lt[(c * RT + t) * LDS + j];
+      li.c[c] = Lt[((K + c) * RT + t) * LDS + j];
+      yr.c[c] = xs[c][j];
+      yi.c[c] = xs[K + c][j];
+      sy.c[c] = xsum[c][j];
+    }
+    Cx<K> p = use3m ? cmul3_pre(lr, li, exp_add(lr, li), yr, yi, sy) : cmul4(lr, li, yr, yi);
     xr = exp_sub(xr, p.re);
     xi = exp_sub(xi, p.im);
   }
-  stexp_<K>(br + i, n, xr);
-  stexp_<K>(bi + i, n, xi);
-}
-
-// Backward substitution, block-diagonal part (rows descending) with the
-// cdiv by U_ii (_kernels.py:753-775).  The blocked order of the
-// off-diagonal subtractions differs from the reference's j-ascending chain,
-// so the solve is tolerance-parity (documented in DESIGN.md).
-template <int K>
-__global__ void bwd_diag_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
-                                int64_t kb, int use3m) {
-  for (int64_t i = r0 + kb - 1; i >= r0; i--) {
-    Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
-    for (int64_t j = i + 1; j < r0 + kb; j++) {
-      Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
-      Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
-      Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
-      xr = exp_sub(xr, p.re);
-      xi = exp_sub(xi, p.im);
-    }
-    Exp<K> ur = ldexp_<K>(F.re + i * F.ld + i, F.ps), ui = ldexp_<K>(F.im + i * F.ld + i, F.ps);
-    Cx<K> q = cdiv(xr, xi, ur, ui);
-    stexp_<K>(br + i, n, q.re);
-    stexp_<K>(bi + i, n, q.im);
-  }
-}
-
-template <int K>
-__global__ void bwd_update_kernel(View F, double* br, double* bi, int64_t n, int64_t r0,
-                                  int64_t kb, int use3m) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= r0) return;
-  Exp<K> xr = ldexp_<K>(br + i, n), xi = ldexp_<K>(bi + i, n);
-  for (int64_t j = r0; j < r0 + kb; j++) {
-    Exp<K> lr = ldexp_<K>(F.re + i * F.ld + j, F.ps), li = ldexp_<K>(F.im + i * F.ld + j, F.ps);
-    Exp<K> yr = ldexp_<K>(br + j, n), yi = ldexp_<K>(bi + j, n);
-    Cx<K> p = cmul(use3m != 0, lr, li, yr, yi);
-    xr = exp_sub(xr, p.re);
-    xi = exp_sub(xi, p.im);
-  }
-  stexp_<K>(br + i, n, xr);
-  stexp_<K>(bi + i, n, xi);
+  stexp_<K>(wr + i, n, xr);
+  stexp_<K>(wi + i, n, xi);
 }
 
 // ===================================================== host-side launchers
@@ -950,6 +1062,46 @@ inline void retain_pool() {
   done[dev] = true;
 }
 
+// The lookahead schedule's high-priority side stream and its two events,
+// released on every exit path (a failed launch throws LaunchError mid-loop).
+struct SideStream {
+  cudaStream_t sp = nullptr;
+  cudaEvent_t ev_narrow = nullptr, ev_panel = nullptr;
+  SideStream() {
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming) != cudaSuccess) {
+      release();
+      throw LaunchError{"side stream / event creation"};
+    }
+  }
+  ~SideStream() { release(); }
+  SideStream(const SideStream&) = delete;
+  SideStream& operator=(const SideStream&) = delete;
+  void release() {
+    if (ev_panel) cudaEventDestroy(ev_panel);
+    if (ev_narrow) cudaEventDestroy(ev_narrow);
+    if (sp) cudaStreamDestroy(sp);
+    sp = nullptr;
+    ev_narrow = ev_panel = nullptr;
+  }
+};
+
+// True the first time a call site asks for the current device (one bit per
+// device in the site's mask): per-function attributes (dynamic shared memory,
+// non-portable clusters) are per device, and the multi-GPU driver launches on
+// several devices from one process.
+inline bool first_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 inline unsigned cdiv_u(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 // SMs of the current device (read once)
 inline int64_t sm_count() {
@@ -977,11 +1129,9 @@ struct Ops {
   static void launch_cfg(const GemmArgs& g, cudaStream_t st, int cls, double ops) {
     using Cfg = GemmCfg<K, MODE, BM_, BN_, BK_, TM_, TN_>;
     auto kern = gemm_kernel<K, MODE, BM_, BN_, BK_, TM_, TN_, MINB_>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static unsigned long long attr_set = 0;
+    if (first_on_device(attr_set))
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-      attr_set = true;
-    }
     dim3 grid((unsigned)((int64_t)cdiv_u(g.l, BN_) * (int64_t)cdiv_u(g.m, BM_)));
     int tok_ = prof_begin(cls, ops, st);
     kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(g);
@@ -1152,6 +1302,10 @@ struct Ops {
                          PanelWs ws, cudaStream_t st) {
     int64_t cend = c0 + w;
     if (int csmax = panel_cluster_size()) {
+      static unsigned long long attr = 0;
+      if (first_on_device(attr))
+        cudaFuncSetAttribute(panel_cluster_kernel<K>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1);
       // smallest power-of-two cluster giving every thread at most one row
       int cs = 1;
       while (cs < csmax &&
@@ -1241,13 +1395,9 @@ struct Ops {
   // sequential schedule); only independent column ranges overlap.
   static void getrf(bool use3m, View A, int64_t n, int64_t Kp, int64_t* piv, PanelWs ws,
                     cudaStream_t st) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStream_t sp;
-    cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi);
-    cudaEvent_t ev_narrow, ev_panel;
-    cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+    SideStream ss;
+    cudaStream_t sp = ss.sp;
+    cudaEvent_t ev_narrow = ss.ev_narrow, ev_panel = ss.ev_panel;
     // MPC_TRACE=1: per-step timeline (stderr) -- where the step time goes
     static const bool trace = getenv("MPC_TRACE") != nullptr;
     std::vector<cudaEvent_t> tev;
@@ -1318,48 +1468,89 @@ struct Ops {
       }
       for (auto e : tev) cudaEventDestroy(e);
     }
-    cudaEventDestroy(ev_narrow);
-    cudaEventDestroy(ev_panel);
-    cudaStreamDestroy(sp);
   }
 
-  static constexpr int SOLVE_BLOCK = 32;
-  // solve_fb (_kernels.py:708-775); b overwritten by x
+  // solve_fb (_kernels.py:708-775); b overwritten by x.  phases: 1 = the
+  // interchanges + forward (unit lower) substitution, 2 = the backward
+  // substitution (b holds the forward result), 3 = both (solve_fb).
   static void getrs(bool use3m, View F, int64_t n, const int64_t* piv, double* br, double* bi,
-                    cudaStream_t st) {
-    int u3 = use3m ? 1 : 0;
-    int tok_ = prof_begin(PC_OTHER, 0.0, st);
-    vec_swap_kernel<K><<<1, 32, 0, st>>>(br, bi, n, piv);
-    prof_end(tok_, st);
-    check_launch("vec_swap_kernel");
-    for (int64_t r0 = 0; r0 < n; r0 += SOLVE_BLOCK) {
-      int64_t kb = std::min<int64_t>(SOLVE_BLOCK, n - r0);
-      int tok_ = prof_begin(PC_OTHER, 0.0, st);
-      fwd_diag_kernel<K><<<1, 1, 0, st>>>(F, br, bi, n, r0, kb, u3);
-      prof_end(tok_, st);
-      check_launch("fwd_diag_kernel");
-      int64_t rest = n - r0 - kb;
-      if (rest > 0) {
-        int tok_ = prof_begin(PC_OTHER, 0.0, st);
-        fwd_update_kernel<K><<<cdiv_u(rest, 128), 128, 0, st>>>(F, br, bi, n, r0, kb, u3);
-        prof_end(tok_, st);
-        check_launch("fwd_update_kernel");
+                    int phases, cudaStream_t st) {
+    if (n <= 0 || phases == 0) return;
+    using C = SolveCfg<K>;
+    const int u3 = use3m ? 1 : 0;
+    const int64_t vec = 2 * (int64_t)K * n;
+    double *y = nullptr, *z = nullptr;
+    int64_t* idx = nullptr;
+    auto ck = [](cudaError_t e, const char* w) {
+      if (e != cudaSuccess) throw LaunchError{w};
+    };
+    struct Free {  // stream-ordered frees on every exit path
+      cudaStream_t st;
+      void* p[3];
+      ~Free() {
+        for (void* q : p)
+          if (q) cudaFreeAsync(q, st);
       }
+    } fr_{st, {nullptr, nullptr, nullptr}};
+    retain_pool();
+    ck(cudaMallocAsync((void**)&y, sizeof(double) * vec, st), "getrs workspace");
+    fr_.p[0] = y;
+    ck(cudaMallocAsync((void**)&z, sizeof(double) * vec, st), "getrs workspace");
+    fr_.p[1] = z;
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) {
+      cudaFuncSetAttribute(trsv_block_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)C::SMEM);
+      cudaFuncSetAttribute(trsv_block_kernel<K, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+      cudaFuncSetAttribute(perm_compose_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
     }
-    int64_t nb = (n + SOLVE_BLOCK - 1) / SOLVE_BLOCK;
-    for (int64_t b = nb - 1; b >= 0; b--) {
-      int64_t r0 = b * SOLVE_BLOCK;
-      int64_t kb = std::min<int64_t>(SOLVE_BLOCK, n - r0);
-      int tok_ = prof_begin(PC_OTHER, 0.0, st);
-      bwd_diag_kernel<K><<<1, 1, 0, st>>>(F, br, bi, n, r0, kb, u3);
+    const unsigned gblocks = (unsigned)std::min<int64_t>(cdiv_u(vec, 256), 148 * 8);
+    if (phases & 1) {
+      ck(cudaMallocAsync((void**)&idx, sizeof(int64_t) * n, st), "getrs workspace");
+      fr_.p[2] = idx;
+      const bool smem = n * (int64_t)sizeof(int) <= 200 * 1024;
+      int tok_ = prof_begin(PC_SOLVE, 0.0, st);
+      perm_compose_kernel<K><<<1, 256, smem ? n * sizeof(int) : 0, st>>>(piv, n, idx,
+                                                                         smem ? 1 : 0);
       prof_end(tok_, st);
-      check_launch("bwd_diag_kernel");
-      if (r0 > 0) {
-        int tok_ = prof_begin(PC_OTHER, 0.0, st);
-        bwd_update_kernel<K><<<cdiv_u(r0, 128), 128, 0, st>>>(F, br, bi, n, r0, kb, u3);
+      check_launch("perm_compose_kernel");
+      tok_ = prof_begin(PC_SOLVE, 0.0, st);
+      perm_gather_kernel<K><<<gblocks, 256, 0, st>>>(br, bi, idx, n, y);
+      prof_end(tok_, st);
+      check_launch("perm_gather_kernel");
+      for (int64_t r0 = 0; r0 < n; r0 += C::KB) {
+        int64_t kb = std::min<int64_t>(C::KB, n - r0);
+        int64_t rows = n - r0 - kb;
+        unsigned grid = rows > 0 ? cdiv_u(rows, C::RT) : 1u;
+        int tok_ = prof_begin(PC_SOLVE, ((double)rows * kb + kb * (kb - 1) / 2.0) * OpModel<K>::upd(use3m), st);
+        trsv_block_kernel<K, true><<<grid, C::RT, C::SMEM, st>>>(F, y, y + K * n, z, z + K * n, n,
+                                                                 r0, kb, u3);
         prof_end(tok_, st);
-        check_launch("bwd_update_kernel");
+        check_launch("trsv_block_kernel<fwd>");
       }
+      if (!(phases & 2)) {
+        ck(cudaMemcpyAsync(br, z, sizeof(double) * K * n, cudaMemcpyDeviceToDevice, st), "getrs copy");
+        ck(cudaMemcpyAsync(bi, z + K * n, sizeof(double) * K * n, cudaMemcpyDeviceToDevice, st),
+           "getrs copy");
+        return;
+      }
+    } else {
+      ck(cudaMemcpyAsync(z, br, sizeof(double) * K * n, cudaMemcpyDeviceToDevice, st), "getrs copy");
+      ck(cudaMemcpyAsync(z + K * n, bi, sizeof(double) * K * n, cudaMemcpyDeviceToDevice, st),
+         "getrs copy");
+    }
+    const int64_t nb = (n + C::KB - 1) / C::KB;
+    for (int64_t b = nb - 1; b >= 0; b--) {
+      int64_t r0 = b * C::KB;
+      int64_t kb = std::min<int64_t>(C::KB, n - r0);
+      unsigned grid = r0 > 0 ? cdiv_u(r0, C::RT) : 1u;
+      int tok_ = prof_begin(PC_SOLVE, ((double)r0 * kb + kb * (kb - 1) / 2.0) * OpModel<K>::upd(use3m), st);
+      trsv_block_kernel<K, false><<<grid, C::RT, C::SMEM, st>>>(F, z, z + K * n, br, bi, n, r0, kb,
+                                                                u3);
+      prof_end(tok_, st);
+      check_launch("trsv_block_kernel<bwd>");
     }
   }
 };

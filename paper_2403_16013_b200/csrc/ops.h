@@ -30,7 +30,7 @@ struct OpsTable {
   void (*getrf)(bool use3m, View A, int64_t n, int64_t Kp, int64_t* piv, PanelWs ws,
                 cudaStream_t st);
   void (*getrs)(bool use3m, View F, int64_t n, const int64_t* piv, double* br, double* bi,
-                cudaStream_t st);
+                int phases, cudaStream_t st);
 };
 
 const OpsTable* ops_k2();

@@ -486,7 +486,8 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
     bool use3m = method == 3;
     mpc::View A{dr, di, n, n * n};
     WsHolder w(k, n, st);
-    if (mpc::resolve_width(k, std::min(K, n), split_bits) < 0)
+    // the budget applies to the trailing update only (none when K >= n)
+    if (n > K && mpc::resolve_width(k, K, split_bits) < 0)
       return fail("dimension exceeds split exactness budget");
     // Same schedule as mpc_getrf (depth-1 lookahead): the narrow update of
     // block b+1, its panel factorization on a high-priority side stream, the
@@ -504,13 +505,9 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
       mpc::cgemm_ozaki_dev(k, use3m, n - end, kw, c1 - c0, A.sub(end, jb), A.sub(jb, c0),
                            A.sub(end, c0), 1, d, mpc::resolve_width(k, kw, split_bits), s);
     };
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStream_t sp;
-    cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi);
-    cudaEvent_t ev_narrow, ev_panel;
-    cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+    mpc::SideStream ss;
+    cudaStream_t sp = ss.sp;
+    cudaEvent_t ev_narrow = ss.ev_narrow, ev_panel = ss.ev_panel;
     // MPC_TRACE=1: per-step timeline on stderr (as mpc_getrf)
     static const bool trace = getenv("MPC_TRACE") != nullptr;
     std::vector<cudaEvent_t> tev;
@@ -575,9 +572,6 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
       }
       for (auto e : tev) cudaEventDestroy(e);
     }
-    cudaEventDestroy(ev_narrow);
-    cudaEventDestroy(ev_panel);
-    cudaStreamDestroy(sp);
     status = w.read_status();
   }
   if (overlap) ho.join(st);

@@ -645,11 +645,11 @@ unsigned grid_for(int64_t total) {
 template <int KL, int CN, int SB>
 void launch_cn(const Params& P, cudaStream_t st, double ops) {
   using T = Tile<KL>;
-  static bool attr = false;
+  static unsigned long long attr = 0;
   auto kern = ozaki_tc_kernel<KL, CN, SB>;
-  if (!attr) {
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-    attr = true;
+    if (CN > 1) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = CN == 1 ? dim3((unsigned)((P.Lp / T::BN) * (P.Mp / BM)))
@@ -789,12 +789,10 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
                    int8_t* out, int64_t Rp, int TR, double* sc) {
     const int stackB = trans;  // right operand: slices stacked per K chunk
     constexpr int KL = decltype(kl)::value;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (first_on_device(attr))
       cudaFuncSetAttribute(split_lines_kernel<KL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
-      attr = true;
-    }
     int NL = 16;  // lines per CTA: as many as fit 200 KB of residual
     while (NL > 1 && (size_t)NL * (size_t)(n | 1) * KL * 8 > SPLIT_SMEM_CAP) NL /= 2;
     const size_t smem = (size_t)NL * (size_t)(n | 1) * KL * 8;

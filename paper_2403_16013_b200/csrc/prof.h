@@ -13,8 +13,9 @@ enum ProfClass {
   PC_PANEL = 2,  // pivot search + column steps
   PC_TRSM = 3,   // TRSM diagonal blocks
   PC_LASWP = 4,  // row interchanges
-  PC_OTHER = 5,  // elementwise, solve, misc
-  PC_N = 6
+  PC_OTHER = 5,  // elementwise, misc
+  PC_SOLVE = 6,  // triangular solves (getrs)
+  PC_N = 7
 };
 
 // Called around every kernel launch.  `ops` is the algorithmic FP64 op count

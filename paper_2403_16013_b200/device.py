@@ -64,13 +64,14 @@ def getrf_ozaki(re, im, piv, K, method="3m", d=None, split_bits=None):
                                                  d, split_bits or 0, _stream(re)), "getrf_ozaki")
 
 
-def getrs(re, im, piv, b_re, b_im, method="3m"):
+def getrs(re, im, piv, b_re, b_im, method="3m", phases=3):
     """solve_fb (lu.py:205-218) on device factors: b ((k, n) tensors) is
-    overwritten with x."""
+    overwritten with x.  phases: 1 = interchanges + forward substitution,
+    2 = backward substitution, 3 = both."""
     k, n, _ = re.shape
-    _lib.check(_lib.lib().mpc_getrs(k, 3 if method == "3m" else 4, n, re.data_ptr(),
-                                    im.data_ptr(), piv.data_ptr(), b_re.data_ptr(),
-                                    b_im.data_ptr(), _stream(re)), "getrs")
+    _lib.check(_lib.lib().mpc_getrs_phases(k, 3 if method == "3m" else 4, n, re.data_ptr(),
+                                           im.data_ptr(), piv.data_ptr(), b_re.data_ptr(),
+                                           b_im.data_ptr(), int(phases), _stream(re)), "getrs")
 
 
 def mat_add(a, b, c, sign=1.0):

@@ -263,7 +263,15 @@ def dist_getrf(backend, comm, lay, k, loc_re, loc_im, piv, lookahead=True):
         if end < n:
             backend.gemm_sub(L11.sub(kw, 0), A.sub(jb, lo), A.sub(end, lo), n - end, kw, M)
 
+    # first singular column, kept on the device: no host synchronisation per
+    # step (the schedule keeps running on a singular panel; the error is
+    # raised once at the end with the first singular column, as lu.py:139-141
+    # reports it)
+    first_sing = backend.empty((1,), "i64")
+    first_sing.fill_(-1)
+
     def check_status(b, bufs, works):
+        nonlocal first_sing
         if asyncp:
             backend.main_wait_side()
         for w in works:
@@ -271,11 +279,9 @@ def dist_getrf(backend, comm, lay, k, loc_re, loc_im, piv, lookahead=True):
                 w.wait()
         meta = bufs[2]
         kw = lay.width(b)
-        st = int(meta[kw].item())
         jb = b * K
         piv[jb:jb + kw].copy_(meta[:kw])
-        if st >= 0:
-            raise SingularMatrixError(st)
+        first_sing = first_sing.where(first_sing >= 0, meta[kw:kw + 1])
 
     bufs, works = panel_step(0)
     for b in range(nb):
@@ -298,6 +304,9 @@ def dist_getrf(backend, comm, lay, k, loc_re, loc_im, piv, lookahead=True):
             bufs, works = nbufs, nworks
     if asyncp:
         backend.main_wait_side()
+    st = int(first_sing.item())
+    if st >= 0:
+        raise SingularMatrixError(st)
     return -1
 
 

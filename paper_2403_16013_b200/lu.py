@@ -109,7 +109,24 @@ def _factor(A, K, method, kc=None):
     im = A.im_plane.data.copy()
     piv = np.arange(n, dtype=np.int64)
     meth = 3 if method == "3m" else 4
-    if n and kc is not None and kc.real_kernel == "ozaki":
+    if n and kc is not None and kc.ngpus > 1:
+        ozk = kc.real_kernel == "ozaki"
+        if ozk and n > K:
+            from .ozaki import _resolve_width
+
+            _resolve_width(k, K, kc.split_bits)
+        st = _lib.check(_lib.lib().mpc_getrf_ngpu(
+            k, meth, n, K, _lib.ptr(re), _lib.ptr(im), _lib.ptr(piv), int(kc.ngpus), 1,
+            1 if ozk else 0, kc.splits_for(k) if ozk else 0,
+            int(kc.split_bits) if (ozk and kc.split_bits is not None) else 0, None),
+            "getrf_ngpu")
+        if st >= 0:
+            raise SingularMatrixError(int(st))
+    elif n and kc is not None and kc.real_kernel == "ozaki":
+        if n > K:  # the split budget binds only when a trailing update runs
+            from .ozaki import _resolve_width
+
+            _resolve_width(k, K, kc.split_bits)
         st = _lib.check(_lib.lib().mpc_getrf_ozaki(
             k, meth, n, K, _lib.ptr(re), _lib.ptr(im), _lib.ptr(piv), kc.splits_for(k),
             int(kc.split_bits) if kc.split_bits is not None else 0, None), "getrf_ozaki")
@@ -223,26 +240,81 @@ def max_rel_err(xhat, x):
     return float(np.max(np.hypot(dr, di) / den)) if x.n else 0.0
 
 
+def _check_inplace_args(re, im, piv):
+    """factor_inplace's buffers: the C side assumes (k, n, n) planes with
+    ld = n, ps = n*n, both on one device (or both host numpy) and an int64
+    pivot vector of length n on the same side."""
+    is_np = isinstance(re, np.ndarray)
+    if is_np != isinstance(im, np.ndarray):
+        raise ValueError("re and im must both be numpy arrays or both CUDA tensors")
+    if len(re.shape) != 3 or re.shape[1] != re.shape[2]:
+        raise ValueError(f"planes must have shape (k, n, n), got {tuple(re.shape)}")
+    if tuple(im.shape) != tuple(re.shape):
+        raise ValueError("re and im shapes differ")
+    if is_np:
+        for name, a in (("re", re), ("im", im)):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError(f"{name} must be C-contiguous float64")
+    else:
+        import torch
+
+        for name, a in (("re", re), ("im", im)):
+            if not isinstance(a, torch.Tensor) or a.dtype != torch.float64 or not a.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float64 tensor")
+            if not a.is_cuda:
+                raise ValueError(f"{name} must be a CUDA tensor (or pass numpy arrays)")
+        if re.device != im.device:
+            raise ValueError("re and im are on different devices")
+    if piv is None:
+        return
+    n = re.shape[1]
+    if is_np:
+        if not isinstance(piv, np.ndarray) or piv.dtype != np.int64 or not piv.flags.c_contiguous:
+            raise ValueError("piv must be a C-contiguous int64 numpy array")
+    else:
+        import torch
+
+        if (not isinstance(piv, torch.Tensor) or piv.dtype != torch.int64
+                or not piv.is_contiguous() or piv.device != re.device):
+            raise ValueError("piv must be a contiguous int64 tensor on the planes' device")
+    if tuple(piv.shape) != (n,):
+        raise ValueError(f"piv must have shape ({n},), got {tuple(piv.shape)}")
+
+
 def factor_inplace(re, im, K, method="3m", piv=None, real_kernel="blocked", d=None,
                    split_bits=None):
     """In-place variant of lu_blocked on raw planar buffers (no copies):
     ``re``/``im`` are (k, n, n) float64 C-contiguous numpy arrays (pinned or
     pageable host memory, staged by the C-ABI) or CUDA tensors (device
-    memory, factored in place on the current stream).  Returns the pivots;
-    raises SingularMatrixError like lu_blocked."""
+    memory, factored in place on the current stream).  ``piv`` (optional) is
+    an int64 vector of length n on the same side; it is allocated there when
+    omitted.  Returns the pivots; raises SingularMatrixError like lu_blocked
+    and ValueError on malformed buffers."""
+    _check_inplace_args(re, im, piv)
     k, n, _ = re.shape
     _check_k(k)
     if not 1 <= K <= max(n, 1):
         raise ValueError(f"panel width K={K} outside [1, {n}]")
-    if piv is None:
-        piv = np.empty(n, dtype=np.int64)
+    if method not in ("3m", "4m"):
+        raise ValueError(f"unknown method {method!r}")
     stream = None
-    if not isinstance(re, np.ndarray):
+    if isinstance(re, np.ndarray):
+        if piv is None:
+            piv = np.empty(n, dtype=np.int64)
+    else:
         import torch
 
+        if piv is None:
+            piv = torch.empty(n, dtype=torch.int64, device=re.device)
         stream = torch.cuda.current_stream(re.device).cuda_stream
+    if n == 0:
+        return piv
     if real_kernel == "ozaki":
+        from .ozaki import _resolve_width
+
         d = d if d is not None else DEFAULT_SPLITS[k]
+        if n > K:  # the budget applies only when a trailing update runs
+            _resolve_width(k, K, split_bits)
         st = _lib.check(_lib.lib().mpc_getrf_ozaki(
             k, 3 if method == "3m" else 4, n, K, _lib.ptr(re), _lib.ptr(im), _lib.ptr(piv), d,
             int(split_bits) if split_bits is not None else 0, stream), "getrf_ozaki")

@@ -88,3 +88,30 @@ def test_oracle_is_not_imported_by_package():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_factor_inplace_validates_buffers():
+    """lu.factor_inplace checks shape, dtype, contiguity, device and piv
+    before any pointer reaches the C-ABI (no GPU needed: it raises first)."""
+    import torch
+
+    from paper_2403_16013_b200 import lu as lum
+
+    n = 8
+    ok = np.zeros((2, n, n))
+    bad_cases = [
+        (np.zeros((2, n, n), dtype=np.float32), ok, None),          # dtype
+        (np.zeros((2, n, n + 1)), np.zeros((2, n, n + 1)), None),   # not square
+        (np.zeros((2, n, n)).transpose(0, 2, 1), ok, None),         # not contiguous
+        (ok, np.zeros((2, n + 1, n + 1)), None),                    # shapes differ
+        (ok, ok.copy(), np.zeros(n, dtype=np.int32)),               # piv dtype
+        (ok, ok.copy(), np.zeros(n - 1, dtype=np.int64)),           # piv length
+        (ok, torch.zeros((2, n, n), dtype=torch.float64), None),    # mixed numpy / tensor
+        (torch.zeros((2, n, n), dtype=torch.float64),               # CPU tensors
+         torch.zeros((2, n, n), dtype=torch.float64), None),
+    ]
+    for re, im, piv in bad_cases:
+        with pytest.raises(ValueError):
+            lum.factor_inplace(re, im, 4, piv=piv)
+    with pytest.raises(ValueError):
+        lum.factor_inplace(ok, ok.copy(), 4, method="5m")

@@ -31,3 +31,34 @@ def test_reference_arm_nonzero_rank_is_silent():
                         "--steps", "1", "--warmup", "0", "--cpu-n", "64"],
                        capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0 and not r.stdout.strip()
+
+
+def test_gpus_n_spawns_n_ranks():
+    """bench.py --gpus 2 (no torchrun around it) starts 2 ranks itself; the
+    dry run exercises that plumbing with gloo on CPU and reports n_gpus = 2."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--dry-run"], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] is True
+    assert sorted(x["rank"] for x in d["ranks"]) == [0, 1]
+    assert len({x["pid"] for x in d["ranks"]}) == 2
+    assert d["max_over_ranks"] == 2.0
+
+
+def test_gpus_n_fails_loudly_without_devices():
+    """--gpus 2 on a box with fewer visible GPUs exits nonzero before spawning."""
+    import torch
+
+    if torch.cuda.device_count() >= 2:
+        import pytest
+
+        pytest.skip("this box has >= 2 GPUs")
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0 and "CUDA device" in r.stderr

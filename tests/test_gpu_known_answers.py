@@ -205,7 +205,8 @@ def test_device_accuracy_report(mp, k):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k,n,K", [(2, 300, 64), (3, 130, 32), (2, 64, 64)])
+@pytest.mark.parametrize("k,n,K", [(2, 300, 64), (3, 130, 32), (2, 64, 64), (2, 520, 32),
+                                   (2, 1000, 48)])
 def test_factor_inplace_pinned_overlap(mp, k, n, K):
     """Host factors in pinned memory: the C-ABI streams finished row blocks
     back while the LU runs (RowSink); the result must equal the pageable
@@ -225,8 +226,8 @@ def test_factor_inplace_pinned_overlap(mp, k, n, K):
     gp = lum.factor_inplace(gr, gi, K)
     dev = torch.device("cuda", 0)
     dr, di = torch.from_numpy(re).to(dev), torch.from_numpy(im).to(dev)
-    dp = torch.empty(n, dtype=torch.int64, device=dev)
-    lum.factor_inplace(dr, di, K, piv=dp)
+    dp = lum.factor_inplace(dr, di, K)  # piv allocated on the planes' device
+    assert isinstance(dp, torch.Tensor) and dp.device == dev
     torch.cuda.synchronize()
     assert np.array_equal(pp, gp) and np.array_equal(pp, dp.cpu().numpy())
     assert pr.numpy().tobytes() == gr.tobytes() == dr.cpu().numpy().tobytes()
@@ -234,7 +235,7 @@ def test_factor_inplace_pinned_overlap(mp, k, n, K):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,K", [(300, 64), (96, 96)])
+@pytest.mark.parametrize("n,K", [(300, 64), (96, 96), (520, 32)])
 def test_factor_inplace_pinned_overlap_ozaki(mp, n, K):
     """The Ozaki LU on pinned host factors (overlapped copies, chunked step-0
     update) equals its device path bit for bit."""

@@ -253,17 +253,104 @@ def test_cfg1_gemm_digest():
         assert digest(C.re_plane.data, C.im_plane.data) == c["digest"], c["method"]
 
 
-def test_cfg2_lu_digest():
+def _rhs_gpu(A, n, k):
+    """b = cgemm_4m(A, x_true) with the naive kernel (the reference's rhs) on the GPU."""
+    xr, xi = problems.x_true(n, k)
+    X = pc(xr.reshape(k, n, 1).copy(), xi.reshape(k, n, 1).copy())
+    B = mp.cgemm_4m(A, X, mp.KernelChoice(method="4m", real_kernel="naive"))
+    return np.array([B.re_plane.data[:, :, 0], B.im_plane.data[:, :, 0]])
+
+
+def _check_lu_case(g, c, re, im):
+    """Pivots and packed factors vs the golden digests; b digest; forward
+    error of the GPU solve within 10x the reference's own (lu.max_rel_err
+    against x_true = 1+1i; the reference's fwd_err is in the golden)."""
+    A = pc(re, im)
+    f = mp.lu_blocked(A, c["K"], kc=mp.KernelChoice(method=c["method"]))
+    assert [int(p) for p in f.pivots] == c["pivots"], c["method"]
+    assert digest(f.packed.re_plane.data, f.packed.im_plane.data) == c["digest"], c["method"]
+    if "digest_planes" in c:
+        k = c["k"]
+        got = [digest(f.packed.re_plane.data[q]) for q in range(k)] + \
+            [digest(f.packed.im_plane.data[q]) for q in range(k)]
+        assert got == c["digest_planes"]
+    if "fwd_err" in c:
+        n, k = c["n"], c["k"]
+        b = _rhs_gpu(A, n, k)
+        assert digest(b) == c["b_digest"]
+        x = mp.solve(f, mp.ComplexVector(b[0], b[1]))
+        fwd = mp.max_rel_err(x, mp.ComplexVector(*problems.x_true(n, k)))
+        assert fwd <= 10 * c["fwd_err"], (c["method"], fwd, c["fwd_err"])
+
+
+@pytest.mark.parametrize("method", ["3m", "4m"])
+def test_cfg2_lu_digest(method):
+    """BASELINE config 2 (n=4096, K=256, DD) in 3M and 4M against the
+    unmodified reference's digests, pivots and forward error."""
     path = os.path.join(GOLD, "cfg2.json")
-    if not os.path.exists(path):
-        pytest.skip("cfg2 golden not generated")
     g = json.load(open(path))
-    c = g["cases"][0]
+    cases = [c for c in g["cases"] if c["method"] == method]
+    assert cases, f"cfg2 {method} golden missing"
+    c = cases[0]
     re, im = problems.lu_matrix(c["n"], c["k"], c["seed"])
     assert digest(re, im) == g["input_digest"]
-    f = mp.lu_blocked(pc(re, im), c["K"], kc=mp.KernelChoice(method=c["method"]))
-    assert [int(p) for p in f.pivots] == c["pivots"]
-    assert digest(f.packed.re_plane.data, f.packed.im_plane.data) == c["digest"]
+    _check_lu_case(g, c, re, im)
+
+
+def test_ill_conditioned_n4096_digest():
+    """Config 4's ill-conditioned input (row i scaled by 10^(-12 i/n)) at
+    n=4096, K=256: pivots, per-plane factor digests and forward error against
+    the unmodified reference (tests/golden/ill_n4096.json)."""
+    g = json.load(open(os.path.join(GOLD, "ill_n4096.json")))
+    c = g["cases"][0]
+    re, im = problems.lu_matrix(c["n"], c["k"], c["seed"], ill_conditioned=True)
+    assert digest(re, im) == g["input_digest"]
+    _check_lu_case(g, c, re, im)
+
+
+@pytest.mark.parametrize("variant", ["uniform", "ill"])
+def test_cfg4_lu_digest(variant):
+    """BASELINE config 4 (n=16384, K=512, DD, 3M), both inputs: pivots and
+    per-plane digests of the packed factors against the pinned CPU oracle's
+    one-time run (oracle/gen_cfg4.py), and the forward error of the GPU
+    solve against the oracle's.  Device path (8 GiB per matrix)."""
+    import torch
+
+    from paper_2403_16013_b200 import device
+
+    path = os.path.join(GOLD, "cfg4.json")
+    if not os.path.exists(path):
+        pytest.skip("cfg4 golden not generated yet (oracle/gen_cfg4.py)")
+    cases = [c for c in json.load(open(path))["cases"] if c["variant"] == variant]
+    if not cases:
+        pytest.skip(f"cfg4 {variant} golden not generated yet")
+    c = cases[0]
+    n, k, K = c["n"], c["k"], c["K"]
+    re, im = problems.lu_matrix(n, k, c["seed"], ill_conditioned=(variant == "ill"))
+    assert digest(re, im) == c["input_digest"]
+    dev = torch.device("cuda", 0)
+    dre, dim_ = torch.from_numpy(re).to(dev), torch.from_numpy(im).to(dev)
+    # b = A x_true (4M, naive chain) on the device before factoring in place
+    xr = torch.zeros((k, n, 1), dtype=torch.float64, device=dev)
+    xr[0] = 1.0
+    br = torch.empty_like(xr)
+    bi = torch.empty_like(xr)
+    device.cgemm(dre, dim_, xr, xr.clone(), br, bi, method="4m")
+    del re, im
+    piv = torch.empty(n, dtype=torch.int64, device=dev)
+    st = device.getrf(dre, dim_, piv, K, "3m")
+    assert st == -1
+    assert [int(p) for p in piv.cpu().tolist()] == c["pivots"]
+    fr, fi = dre.cpu().numpy(), dim_.cpu().numpy()
+    got = [digest(fr[q]) for q in range(k)] + [digest(fi[q]) for q in range(k)]
+    assert got == c["digest_planes"]
+    b = torch.stack([br.reshape(k, n), bi.reshape(k, n)]).cpu().numpy()
+    assert digest(b) == c["b_digest"]
+    br2, bi2 = br.reshape(k, n).contiguous(), bi.reshape(k, n).contiguous()
+    device.getrs(dre, dim_, piv, br2, bi2, "3m")
+    x = mp.ComplexVector(br2.cpu().numpy(), bi2.cpu().numpy())
+    fwd = mp.max_rel_err(x, mp.ComplexVector(*problems.x_true(n, k)))
+    assert fwd <= 10 * c["fwd_err"], (fwd, c["fwd_err"])
 
 
 @pytest.mark.parametrize("k", [3, 4])
