@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-accuracy", action="store_true",
                    help="skip the forward / backward error report")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-dropin", action="store_true",
+                   help="skip the lu_blocked-on-pageable-numpy end-to-end timing")
     p.add_argument("--no-prof", action="store_true")
     p.add_argument("--no-alt", action="store_true",
                    help="skip the secondary measurement with the other real kernel")
@@ -209,11 +211,47 @@ def cpu_lu_gflops(n, K, k, method, seed, reps=1):
     return conv_flops(n) / t / 1e9, threads, t
 
 
+def host_info():
+    """nproc and the CPU model (lscpu) of the host the CPU legs run on."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            key, _, val = line.partition(":")
+            if key.strip() in ("Model name", "Socket(s)", "Core(s) per socket",
+                               "Thread(s) per core"):
+                info[key.strip()] = val.strip()
+    except Exception as e:  # lscpu missing: record why
+        info["lscpu"] = f"unavailable: {e}"
+    return info
+
+
+def cpu_baseline_cfg2(args):
+    """SURVEY.md §8d protocol: the reference algorithm (oracle C port, all host
+    threads) on the config-2 shape (n=4096, K=256, same k / method / seed
+    family) in the same job; config 4 (~3 h of CPU) is reported as that time
+    x 64 (8n^3/3 scales by 64 from n=4096 to 16384), labelled extrapolated --
+    its GFLOP/s equals the measured config-2 rate."""
+    n2, K2 = (4096, 256) if args.n >= 4096 else (args.n, min(args.K, args.n))
+    g, threads, t = cpu_lu_gflops(n2, K2, args.k, args.method, args.seed)
+    scale = (args.n / n2) ** 3
+    return {"value": g, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle C port of lu._factor (OpenMP, {threads} threads) on the config-2 "
+                       f"shape n={n2} K={K2} {args.method}: {t:.1f} s measured in this job; "
+                       f"n={args.n} K={args.K} extrapolated x{scale:.0f} = {t * scale:.0f} s "
+                       "(not run)"),
+            "measured": {"n": n2, "K": K2, "seconds": t},
+            "extrapolated": {"n": args.n, "K": args.K, "seconds": t * scale, "factor": scale},
+            "host": host_info()}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     n = min(args.cpu_n, args.n)
-    K = min(args.K, n)
+    # same K / n as the workload (config 4: 512 / 16384 = 1/32), so the
+    # sample's panel / TRSM / trailing-GEMM op split matches the workload's
+    K = max(1, min(n, round(args.K * n / args.n)))
     for _ in range(args.warmup):
         cpu_lu_gflops(min(n, 256), min(K, 256), args.k, args.method, args.seed)
     vals, secs = [], []
@@ -223,8 +261,10 @@ def run_reference(args, rank, world):
         vals.append(g)
         secs.append(t)
     value = statistics.median(vals)
-    sample = (f"complex {'DD' if args.k == 2 else 'k=%d' % args.k} blocked LU n={n} K={K} "
-              f"{args.method} (bounded sample of the {args.n} workload)")
+    sample = (f"oracle C port of lu._factor (OpenMP, {threads} threads): complex "
+              f"{'DD' if args.k == 2 else 'k=%d' % args.k} blocked LU n={n} K={K} {args.method}, "
+              f"{statistics.median(secs):.1f} s per step (bounded sample of the n={args.n} "
+              f"K={args.K} workload at the same K/n)")
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -233,7 +273,7 @@ def run_reference(args, rank, world):
         "config": {"workload": workload(args), "n": args.n, "K": args.K, "k": args.k,
                    "method": args.method, "cpu_sample_n": n},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "host": host_info()},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -411,13 +451,26 @@ def run_b200(args, rank, world):
         acc["seconds"] = time.perf_counter() - a0
         acc["factor_kernel"] = args.real_kernel
 
+    # the drop-in API exactly as a reference user calls it: lu_blocked on a
+    # PlanarComplexMatrix of ordinary (pageable) numpy planes -- host copy of
+    # A (lu.py:132-133 semantics), staged H2D, factor, D2H; wall clock
+    e2e_dropin = None
+    if not args.no_e2e and not args.no_dropin:
+        A = mp.PlanarComplexMatrix(mp.RealMatrix(re0), mp.RealMatrix(im0))
+        kc = mp.KernelChoice(method=args.method, real_kernel=args.real_kernel)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        f = mp.lu_blocked(A, K, kc=kc)
+        wt = time.perf_counter() - w0
+        e2e_dropin = {"value": conv_flops(n) / wt / 1e9, "unit": "GFLOP/s", "seconds": wt,
+                      "api": "paper_2403_16013_b200.lu_blocked(PlanarComplexMatrix, K, kc) on "
+                             "pageable numpy planes (wall clock, one call)",
+                      "pivots_match_device_run": bool(np.array_equal(f.pivots, piv.cpu().numpy()))}
+        del f, A
+
     cpu = None
     if not args.no_cpu:
-        g, threads, t = cpu_lu_gflops(min(args.cpu_n, n), min(K, args.cpu_n), k, args.method,
-                                      args.seed)
-        cpu = {"value": g, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-               "sample": f"oracle C port of lu._factor, n={min(args.cpu_n, n)} K={min(K, args.cpu_n)} "
-                         f"{args.method}, {t:.1f} s on {threads} threads"}
+        cpu = cpu_baseline_cfg2(args)
 
     # secondary measurement: the same factorization with the other real
     # kernel of KernelChoice (blocked EFT FP64 <-> Ozaki on the INT8 tensor
@@ -477,7 +530,7 @@ def run_b200(args, rank, world):
         "fp64_pct_of_measured_peak": fp64_pct,
         "int8_peak_measured_tops": peak_i8 / 1e12 if peak_i8 else None,
         "fp64_peak_measured_tops": peak / 1e12,
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin, "clocks": clk,
         "gpu_launches": int(launches), "breakdown": breakdown, "alt_real_kernel": alt,
         "accuracy": acc,
     }

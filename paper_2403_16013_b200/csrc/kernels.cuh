@@ -887,18 +887,36 @@ struct SolveCfg {
 //   * diagonal block (every CTA, redundantly, in warp 0): lane r holds x_r;
 //     FWD: for s ascending, x_s is final, broadcast by shuffle, lanes r > s
 //     apply x_r -= cmul(L_rs, x_s) -- exactly the reference's chain order
-//     (j ascending); BWD: for s descending, lane s divides by U_ss, then
-//     lanes r < s apply x_r -= cmul(U_rs, x_s).
+//     (j ascending); BWD: for s descending, lane s scales by the precomputed
+//     reciprocal z_s = cdiv(1, U_ss) (the reference divides, cdiv(x_s, U_ss):
+//     one cdiv per row would sit on the sequential critical path, n deep),
+//     then lanes r < s apply x_r -= cmul(U_rs, x_s).
 //   * off-diagonal rows: one thread per row, x_i -= cmul(F_ij, x_j) for j
 //     ascending over the block, F tile staged coalesced in shared memory.
 // Forward chains therefore equal the reference's (blocks ascending, j
 // ascending within each): bitwise.  Backward applies blocks in descending
 // order -- the reference's row chain (j ascending up to n) is inherently
-// sequential (n^2/2 dependent steps) -- so it is tolerance-parity.
+// sequential (n^2/2 dependent steps) -- and multiplies by reciprocals, so it
+// is tolerance-parity.
+//
+// diag_inv_kernel: z_i = cdiv(1, U_ii) for every row (cdiv_core,
+// _kernels.py:549-561), one thread per row.
+template <int K>
+__global__ void diag_inv_kernel(View F, int64_t n, double* inv, int use3m) {
+  (void)use3m;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Exp<K> one = exp_zero<K>(), zero = exp_zero<K>();
+  one.c[0] = 1.0;
+  Exp<K> ur = ldexp_<K>(F.re + i * F.ld + i, F.ps), ui = ldexp_<K>(F.im + i * F.ld + i, F.ps);
+  Cx<K> z = cdiv(one, zero, ur, ui);
+  stexp_<K>(inv + i, n, z.re);
+  stexp_<K>(inv + K * n + i, n, z.im);
+}
 template <int K, bool FWD>
 __global__ void __launch_bounds__(SolveCfg<K>::RT)
     trsv_block_kernel(View F, double* wr, double* wi, double* fr, double* fi, int64_t n,
-                      int64_t r0, int64_t kb, int use3m) {
+                      int64_t r0, int64_t kb, int use3m, const double* __restrict__ inv) {
   using C = SolveCfg<K>;
   constexpr int KB = C::KB, RT = C::RT, LDS = C::LDS;
   extern __shared__ double sm[];
@@ -910,23 +928,32 @@ __global__ void __launch_bounds__(SolveCfg<K>::RT)
   const int64_t row0 = FWD ? r0 + kb + (int64_t)blockIdx.x * RT : (int64_t)blockIdx.x * RT;
   const int64_t rowEnd = FWD ? n : r0;
   // staging with cp.async (no register round trip, every load in flight at
-  // once): group 0 = the diagonal block, group 1 = the off-diagonal rows,
-  // which keep landing while warp 0 solves the diagonal block
-  for (int e = t; e < 2 * K * KB * KB; e += RT) {
-    int q = e / (KB * KB), rr = (e / KB) % KB, jj = e % KB;
-    const double* base = q < K ? F.re + q * F.ps : F.im + (q - K) * F.ps;
-    bool ok = rr < kb && jj < kb;
-    cp_async8(&Ld[(q * KB + rr) * LDS + jj], ok ? base + (r0 + rr) * F.ld + r0 + jj : base, ok);
+  // once), lane = column of the 32-wide block: group 0 = the diagonal block,
+  // group 1 = the off-diagonal rows, which keep landing while warp 0 solves
+  // the diagonal block
+  {
+    const int lane = t & 31, wid = t >> 5;
+    constexpr int NW = RT / 32;
+    const bool colok = lane < kb;
+#pragma unroll
+    for (int q = 0; q < 2 * K; q++) {
+      const double* base = (q < K ? F.re + q * F.ps : F.im + (q - K) * F.ps) + r0 + lane;
+      for (int rr = wid; rr < KB; rr += NW) {
+        const bool ok = colok && rr < kb;
+        cp_async8(&Ld[(q * KB + rr) * LDS + lane], ok ? base + (r0 + rr) * F.ld : base, ok);
+      }
+    }
+    cp_async_commit();
+#pragma unroll
+    for (int q = 0; q < 2 * K; q++) {
+      const double* base = (q < K ? F.re + q * F.ps : F.im + (q - K) * F.ps) + r0 + lane;
+      for (int rr = wid; rr < RT; rr += NW) {
+        const bool ok = colok && row0 + rr < rowEnd;
+        cp_async8(&Lt[(q * RT + rr) * LDS + lane], ok ? base + (row0 + rr) * F.ld : base, ok);
+      }
+    }
+    cp_async_commit();
   }
-  cp_async_commit();
-  for (int e = t; e < 2 * K * RT * KB; e += RT) {
-    int q = e / (RT * KB), rr = (e / KB) % RT, jj = e % KB;
-    int64_t i = row0 + rr;
-    const double* base = q < K ? F.re + q * F.ps : F.im + (q - K) * F.ps;
-    bool ok = i < rowEnd && jj < kb;
-    cp_async8(&Lt[(q * RT + rr) * LDS + jj], ok ? base + i * F.ld + r0 + jj : base, ok);
-  }
-  cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
   if (t < 32) {
@@ -961,11 +988,16 @@ __global__ void __launch_bounds__(SolveCfg<K>::RT)
         }
       }
     } else {
+      // z_r = 1 / U_rr (cdiv, precomputed for every row by diag_inv_kernel,
+      // off the critical path): x_s = cmul(x_s, z_s) at step s
+      Exp<K> zr = exp_zero<K>(), zi = exp_zero<K>();
+      if (live) {
+        zr = ldexp_<K>(inv + r0 + r, n);
+        zi = ldexp_<K>(inv + K * n + r0 + r, n);
+      }
       for (int s = (int)kb - 1; s >= 0; s--) {
         if (r == s) {
-          Exp<K> ur, ui;
-          ld_d(s, s, ur, ui);
-          Cx<K> q = cdiv(xr, xi, ur, ui);
+          Cx<K> q = cmul(use3m != 0, xr, xi, zr, zi);
           xr = q.re;
           xi = q.im;
         }
@@ -1479,19 +1511,19 @@ struct Ops {
     using C = SolveCfg<K>;
     const int u3 = use3m ? 1 : 0;
     const int64_t vec = 2 * (int64_t)K * n;
-    double *y = nullptr, *z = nullptr;
+    double *y = nullptr, *z = nullptr, *inv = nullptr;
     int64_t* idx = nullptr;
     auto ck = [](cudaError_t e, const char* w) {
       if (e != cudaSuccess) throw LaunchError{w};
     };
     struct Free {  // stream-ordered frees on every exit path
       cudaStream_t st;
-      void* p[3];
+      void* p[4];
       ~Free() {
         for (void* q : p)
           if (q) cudaFreeAsync(q, st);
       }
-    } fr_{st, {nullptr, nullptr, nullptr}};
+    } fr_{st, {nullptr, nullptr, nullptr, nullptr}};
     retain_pool();
     ck(cudaMallocAsync((void**)&y, sizeof(double) * vec, st), "getrs workspace");
     fr_.p[0] = y;
@@ -1526,7 +1558,7 @@ struct Ops {
         unsigned grid = rows > 0 ? cdiv_u(rows, C::RT) : 1u;
         int tok_ = prof_begin(PC_SOLVE, ((double)rows * kb + kb * (kb - 1) / 2.0) * OpModel<K>::upd(use3m), st);
         trsv_block_kernel<K, true><<<grid, C::RT, C::SMEM, st>>>(F, y, y + K * n, z, z + K * n, n,
-                                                                 r0, kb, u3);
+                                                                 r0, kb, u3, nullptr);
         prof_end(tok_, st);
         check_launch("trsv_block_kernel<fwd>");
       }
@@ -1541,6 +1573,14 @@ struct Ops {
       ck(cudaMemcpyAsync(z + K * n, bi, sizeof(double) * K * n, cudaMemcpyDeviceToDevice, st),
          "getrs copy");
     }
+    ck(cudaMallocAsync((void**)&inv, sizeof(double) * vec, st), "getrs workspace");
+    fr_.p[3] = inv;
+    {
+      int tok_ = prof_begin(PC_SOLVE, 0.0, st);
+      diag_inv_kernel<K><<<cdiv_u(n, 128), 128, 0, st>>>(F, n, inv, u3);
+      prof_end(tok_, st);
+      check_launch("diag_inv_kernel");
+    }
     const int64_t nb = (n + C::KB - 1) / C::KB;
     for (int64_t b = nb - 1; b >= 0; b--) {
       int64_t r0 = b * C::KB;
@@ -1548,7 +1588,7 @@ struct Ops {
       unsigned grid = r0 > 0 ? cdiv_u(r0, C::RT) : 1u;
       int tok_ = prof_begin(PC_SOLVE, ((double)r0 * kb + kb * (kb - 1) / 2.0) * OpModel<K>::upd(use3m), st);
       trsv_block_kernel<K, false><<<grid, C::RT, C::SMEM, st>>>(F, z, z + K * n, br, bi, n, r0, kb,
-                                                                u3);
+                                                                u3, inv);
       prof_end(tok_, st);
       check_launch("trsv_block_kernel<bwd>");
     }
