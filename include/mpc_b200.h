@@ -179,6 +179,12 @@ int mpc_cgemm_ozaki(int k, int method, int64_t m, int64_t n, int64_t l,
 int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, double* im,
                         int64_t* piv, int d, int split_bits, void* stream);
 
+/* Page-lock (cudaHostRegister) / release an existing host range, so the LU
+ * entry points overlap its copies with the factorization (the drop-in
+ * lu_blocked registers its output copy of A for the call). */
+int mpc_host_register(void* p, int64_t bytes);
+int mpc_host_unregister(void* p);
+
 /* ---- measurement hooks (bench.py) ---- */
 /* Per-launch CUDA-event timing of the kernel classes whose bit is set in
  * `mask` (bit c = class c below; 0 disables).  Clears previous records. */

@@ -22,6 +22,7 @@ from .cmatrix import (
     rgemm_strassen,
 )
 from .lu import (
+    ComplexScalar,
     ComplexVector,
     LinearSystem,
     LUFactors,

@@ -33,6 +33,8 @@ _SIGS = {
     "mpc_laswp": (_i, [_i, _i64, _p, _p, _i64, _i64, _p, _i64, _i64, _p]),
     "mpc_getrf": (_i64, [_i, _i, _i64, _i64, _p, _p, _p, _p]),
     "mpc_getrs": (_i, [_i, _i, _i64, _p, _p, _p, _p, _p, _p]),
+    "mpc_host_register": (_i, [_p, _i64]),
+    "mpc_host_unregister": (_i, [_p]),
     "mpc_getrf_ngpu": (ctypes.c_int64, [_i, _i, _i64, _i64, _p, _p, _p, _i, _i, _i, _i, _i, _p]),
     "mpc_getrs_phases": (_i, [_i, _i, _i64, _p, _p, _p, _p, _p, _i, _p]),
     "mpc_ozaki_split": (_i, [_i, _i64, _i64, _p, _i64, _i64, _i, _i, _i, _p, _p, _p]),

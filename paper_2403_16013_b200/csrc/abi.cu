@@ -421,6 +421,21 @@ int64_t mpc_getrf(int k, int method, int64_t n, int64_t K, double* re, double* i
   MPC_CATCH
 }
 
+int mpc_host_register(void* p, int64_t bytes) {
+  if (p == nullptr || bytes <= 0) return fail("bad host range");
+  MPC_TRY
+  ck(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault), "cudaHostRegister");
+  return 0;
+  MPC_CATCH
+}
+
+int mpc_host_unregister(void* p) {
+  MPC_TRY
+  ck(cudaHostUnregister(p), "cudaHostUnregister");
+  return 0;
+  MPC_CATCH
+}
+
 int mpc_getrs(int k, int method, int64_t n, const double* re, const double* im,
               const int64_t* piv, double* b_re, double* b_im, void* stream) {
   return mpc_getrs_phases(k, method, n, re, im, piv, b_re, b_im, 3, stream);

@@ -31,7 +31,9 @@ MPC_DI double dmul(double a, double b) { return __dmul_rn(a, b); }
 
 MPC_DI uint64_t bits(double x) { return (uint64_t)__double_as_longlong(x); }
 MPC_DI uint64_t absbits(double x) { return bits(x) & 0x7FFFFFFFFFFFFFFFull; }
-MPC_DI bool is_nonzero(double x) { return absbits(x) != 0ull; }
+// x != 0 (either sign); NaN counts as nonzero, like the bit test it replaces
+// (one DSETP on the FP64 pipe instead of integer compare work)
+MPC_DI bool is_nonzero(double x) { return x != 0.0; }
 
 // ---------------------------------------------------------------- EFTs
 // _kernels.py:28-34
@@ -186,9 +188,10 @@ MPC_DI void vecsum_extract(double (&buf)[M], int m, Exp<K>& out) {
           eps = r;
           done = true;
         } else {
+          // j <= K - 2 here, and j <= i: only those slots can take r
 #pragma unroll
-          for (int q = 0; q < K; q++)
-            if (q == j) out.c[q] = r;
+          for (int q = 0; q < K - 1; q++)
+            if (q <= i && q == j) out.c[q] = r;
           j++;
           eps = enew;
         }
@@ -257,14 +260,6 @@ MPC_DI void net_at(F&& ce) {
   SortNet<N>::apply([&](int a, int b) { ce(a + OFF, b + OFF); });
 }
 
-template <int M>
-MPC_DI bool keys_sorted(const uint64_t (&key)[M]) {
-  bool ok = true;
-#pragma unroll
-  for (int i = 0; i + 1 < M; i++) ok = ok && key[i] >= key[i + 1];
-  return ok;
-}
-
 // merge networks for two sorted runs of K (positions [0, K) and [K, 2K)),
 // 0-1 verified over all pairs of sorted runs
 template <int K>
@@ -320,20 +315,44 @@ struct DivBands {
   }
 };
 
+// a strictly precedes b in _sort_desc's order (|v| desc, then v desc),
+// compared on the FP64 pipe (DSETP with |.| operand modifiers); zeros of
+// either sign compare equal, as in the reference's insertion sort
+MPC_DI bool precedes(double a, double b) {
+  const double fa = fabs(a), fb = fabs(b);
+  return fa > fb || (fa == fb && a > b);
+}
+
+// Structured sort of a full term list (every slot a real term): the
+// caller's presort network runs with a magnitude-only comparator (one DSETP
+// + the selects of the swap), the result is checked pair by pair in the
+// exact order, and only an unsorted result (bands overlap, or two terms of
+// equal magnitude and opposite sign) runs the exact full network.  Any
+// permutation sorts to the same sequence up to the order of zeros, which
+// cannot change the VecSum sweep (see sort_key), so renorm's bits do not
+// depend on which path ran.  Doubles are compared directly: no key
+// construction / reconstruction (the integer compare-and-select of the key
+// network was the issue bottleneck of the TD / QD kernels, ncu r2).
 template <int M, typename Pre>
 MPC_DI void sort_desc_pre(double (&buf)[M], Pre&& pre) {
-  uint64_t key[M];
-#pragma unroll
-  for (int i = 0; i < M; i++) key[i] = sort_key(buf[i]);
-  auto ce = [&](int a, int b) {
-    const uint64_t ka = key[a], kb = key[b];
-    key[a] = ka > kb ? ka : kb;
-    key[b] = ka > kb ? kb : ka;
+  auto ce_abs = [&](int a, int b) {
+    const double va = buf[a], vb = buf[b];
+    const bool sw = fabs(vb) > fabs(va);
+    buf[a] = sw ? vb : va;
+    buf[b] = sw ? va : vb;
   };
-  pre(ce);
-  if (!keys_sorted<M>(key)) SortNet<M>::apply(ce);
+  pre(ce_abs);
+  bool bad = false;
 #pragma unroll
-  for (int i = 0; i < M; i++) buf[i] = from_key(key[i]);
+  for (int i = 0; i + 1 < M; i++) bad |= precedes(buf[i + 1], buf[i]);
+  if (bad) {
+    SortNet<M>::apply([&](int a, int b) {
+      const double va = buf[a], vb = buf[b];
+      const bool sw = precedes(vb, va);
+      buf[a] = sw ? vb : va;
+      buf[b] = sw ? va : vb;
+    });
+  }
 }
 
 // renorm, _kernels.py:124-139 on buf[0..m) (buf clobbered)

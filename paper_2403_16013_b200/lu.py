@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _lib
 from .cmatrix import DEFAULT_SPLITS, KernelChoice, PlanarComplexMatrix, _check_k
-from .rmatrix import RealMatrix, check_threads
+from .rmatrix import Expansion, RealMatrix, check_threads
 
 
 class SingularMatrixError(ValueError):
@@ -24,6 +24,38 @@ class SingularMatrixError(ValueError):
     def __init__(self, column):
         super().__init__(f"singular matrix at column {column}")
         self.column = column
+
+
+class ComplexScalar:
+    """Value holder for one complex expansion (cscalar.py surface: re, im,
+    from_complex, to_complex); the scalar arithmetic API is outside the hot
+    path (DESIGN.md)."""
+
+    __slots__ = ("re", "im")
+
+    def __init__(self, re, im):
+        if re.k != im.k:
+            raise ValueError("re and im must share the component count")
+        self.re = re
+        self.im = im
+
+    @property
+    def k(self):
+        return self.re.k
+
+    @classmethod
+    def from_complex(cls, z, k):
+        z = complex(z)
+        return cls(Expansion.from_float(z.real, k), Expansion.from_float(z.imag, k))
+
+    def to_complex(self):
+        return complex(self.re.to_float(), self.im.to_float())
+
+    def __eq__(self, other):
+        return isinstance(other, ComplexScalar) and self.re == other.re and self.im == other.im
+
+    def __repr__(self):
+        return f"ComplexScalar({self.re!r}, {self.im!r})"
 
 
 class ComplexVector:
@@ -53,6 +85,15 @@ class ComplexVector:
 
     def copy(self):
         return ComplexVector(self.re.copy(), self.im.copy())
+
+    def at(self, i):
+        return ComplexScalar(Expansion(self.re[:, i].copy()), Expansion(self.im[:, i].copy()))
+
+    def set_at(self, i, z):
+        if z.re.k != self.k or z.im.k != self.k:
+            raise ValueError("component count mismatch")
+        self.re[:, i] = z.re.components
+        self.im[:, i] = z.im.components
 
     def bitwise_equal(self, other):
         return bool(np.array_equal(self.re, other.re) and np.array_equal(self.im, other.im))
@@ -101,13 +142,64 @@ class LUFactors:
         return U
 
 
+# output copies at least this large are page-locked for the call, so the
+# C-ABI overlaps their host<->device copies with the factorization
+# (HostOverlap); below it the staged copies cost less than registering
+_REGISTER_BYTES = 64 << 20
+
+
+def _par_copy(src):
+    """np.copy of a large (k, n, n) plane stack with one thread per row chunk
+    (numpy releases the GIL in copyto): the single-threaded copy costs ~1 s
+    per 8 GiB."""
+    import concurrent.futures as cf
+    import os
+
+    out = np.empty_like(src)
+    nt = min(16, os.cpu_count() or 1)
+    rows = src.shape[1]
+    ch = (rows + nt - 1) // nt
+    with cf.ThreadPoolExecutor(nt) as ex:
+        list(ex.map(lambda i: np.copyto(out[:, i * ch:(i + 1) * ch], src[:, i * ch:(i + 1) * ch]),
+                    range(nt)))
+    return out
+
+
+class _Pinned:
+    """cudaHostRegister the factor copies for the duration of the call."""
+
+    def __init__(self, arrays):
+        self.done = []
+        for a in arrays:
+            if a.nbytes >= _REGISTER_BYTES and _lib.lib().mpc_host_register(_lib.ptr(a), a.nbytes) == 0:
+                self.done.append(a)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        for a in self.done:
+            _lib.lib().mpc_host_unregister(_lib.ptr(a))
+        return False
+
+
 def _factor(A, K, method, kc=None):
-    """lu._factor (lu.py:129-163) as one device call."""
+    """lu._factor (lu.py:129-163) as one device call, on copies of A's
+    planes (lu.py:132-133); large copies are page-locked for the call so the
+    input / output transfers overlap the factorization."""
     n, k = A.rows, A.k
     _check_k(k)
-    re = A.re_plane.data.copy()
-    im = A.im_plane.data.copy()
+    big = A.re_plane.data.nbytes >= _REGISTER_BYTES
+    re = _par_copy(A.re_plane.data) if big else A.re_plane.data.copy()
+    im = _par_copy(A.im_plane.data) if big else A.im_plane.data.copy()
     piv = np.arange(n, dtype=np.int64)
+    with _Pinned([re, im]):
+        _factor_device(re, im, piv, n, k, K, method, kc)
+    packed = PlanarComplexMatrix(RealMatrix(re), RealMatrix(im))
+    return LUFactors(packed=packed, pivots=piv, method=method)
+
+
+def _factor_device(re, im, piv, n, k, K, method, kc):
     meth = 3 if method == "3m" else 4
     if n and kc is not None and kc.ngpus > 1:
         ozk = kc.real_kernel == "ozaki"
@@ -137,8 +229,6 @@ def _factor(A, K, method, kc=None):
                                              _lib.ptr(im), _lib.ptr(piv), None), "getrf")
         if st >= 0:
             raise SingularMatrixError(int(st))
-    packed = PlanarComplexMatrix(RealMatrix(re), RealMatrix(im))
-    return LUFactors(packed=packed, pivots=piv, method=method)
 
 
 def lu_normal(A, threads=1, method="3m"):

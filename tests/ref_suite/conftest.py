@@ -1,0 +1,107 @@
+"""Runs the REFERENCE's own API tests (pkg/tests/test_cgemm.py, test_rgemm.py,
+test_lu.py, test_ozaki.py, renamed test_ref_*; copied by
+tools/vendor_ref_suite.py into the git-ignored _vendored/ directory) against
+this package, SURVEY.md §7.2 / VERDICT r1 item 8.
+
+TEST INFRASTRUCTURE ONLY.  ``import mpclu`` resolves to
+paper_2403_16013_b200 (the hot-path API: containers, KernelChoice, cgemm,
+rgemm, mat_add, LU, TRSM, solve, Ozaki, error metrics -- all on the GPU).
+The reference's SCALAR expansion arithmetic (exp_add / exp_mul /
+renormalize / nonoverlapping on single expansions), which its tests use only
+to build expected values, is outside the hot path; here it is
+served by the CPU oracle (oracle/, itself pinned to the reference), the
+checker -- never by the package.
+
+Skipped (documented): tests of out-of-scope pieces -- Strassen (square-only
+in the reference; its LU variant always fails there), and the
+threads-as-parallelism knobs of the CPU kernels.  Everything else runs as
+written.  All tests here need the GPU (marked gpu)."""
+
+import os
+import sys
+import types
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import paper_2403_16013_b200 as _pkg  # noqa: E402
+from paper_2403_16013_b200 import cmatrix, harness, lu, ozaki, rmatrix  # noqa: E402
+from paper_2403_16013_b200.rmatrix import Expansion  # noqa: E402
+
+# out-of-scope tests (name substrings) -> reason
+SKIP = {
+    "strassen": "Strassen is outside the B200 hot path (square-only in the reference; DESIGN.md)",
+}
+
+
+def _orc():
+    from oracle import oracle
+
+    oracle.build()
+    return oracle
+
+
+def _exp_binop(name):
+    def f(x, y):
+        if x.k != y.k:
+            raise ValueError("component count mismatch")
+        return Expansion(getattr(_orc(), name)(x.components, y.components))
+    f.__name__ = name
+    return f
+
+
+def _renormalize(raw, k):
+    return Expansion(_orc().renorm(np.asarray(raw, dtype=np.float64), k))
+
+
+def _nonoverlapping(arr):
+    return _orc().nonoverlapping(np.asarray(arr, dtype=np.float64))
+
+
+def _install():
+    m = types.ModuleType("mpclu")
+    m.__dict__.update({k: v for k, v in vars(_pkg).items() if not k.startswith("__")})
+    m.nonoverlapping = _nonoverlapping
+    m.__path__ = []  # a package, so "mpclu.x" submodules resolve through sys.modules
+    exp = types.ModuleType("mpclu.expansion")
+    exp.__dict__.update({k: v for k, v in vars(_pkg.expansion).items() if not k.startswith("__")})
+    exp.Expansion = Expansion
+    exp.exp_add = _exp_binop("exp_add")
+    exp.exp_sub = _exp_binop("exp_sub")
+    exp.exp_mul = _exp_binop("exp_mul")
+    exp.exp_div = _exp_binop("exp_div")
+    exp.renormalize = _renormalize
+    exp.nonoverlapping = _nonoverlapping
+    kern = types.ModuleType("mpclu._kernels")
+    kern.renorm_planes = lambda R, k: rmatrix.renorm_planes(R)
+    mods = {"mpclu": m, "mpclu.expansion": exp, "mpclu._kernels": kern,
+            "mpclu.rmatrix": rmatrix, "mpclu.cmatrix": cmatrix, "mpclu.lu": lu,
+            "mpclu.ozaki": ozaki, "mpclu.bench": harness}
+    for name, mod in mods.items():
+        sys.modules[name] = mod
+        if "." in name:
+            setattr(m, name.split(".", 1)[1], mod)
+
+
+_install()
+
+
+@pytest.fixture
+def rng():
+    """The reference conftest's fixture (pkg/tests/conftest.py)."""
+    return np.random.default_rng(20240801)
+
+
+def pytest_collection_modifyitems(config, items):
+    for it in items:
+        if "ref_suite" not in str(it.fspath):
+            continue
+        it.add_marker(pytest.mark.gpu)
+        for key, why in SKIP.items():
+            if key in it.nodeid.lower():
+                it.add_marker(pytest.mark.skip(reason=why))

@@ -9,7 +9,7 @@ import re
 import numpy as np
 import pytest
 
-from conftest import ROOT
+from testpaths import ROOT
 
 HEADER = os.path.join(ROOT, "include", "mpc_b200.h")
 

@@ -5,7 +5,7 @@ import os
 import subprocess
 import sys
 
-from conftest import ROOT
+from testpaths import ROOT
 
 
 def test_reference_arm_json():

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from conftest import ROOT
+from testpaths import ROOT
 
 
 def _free_port():

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from conftest import ROOT
+from testpaths import ROOT
 
 pytestmark = pytest.mark.gpu
 

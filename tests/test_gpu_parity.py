@@ -9,7 +9,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLD
+from testpaths import GOLD
 
 pytestmark = pytest.mark.gpu
 

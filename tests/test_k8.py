@@ -9,7 +9,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLD
+from testpaths import GOLD
 
 CASES = [("dd", 12), ("dd", 7), ("td", 10), ("qd", 9)]
 K_OF = {"dd": 2, "td": 3, "qd": 4}

@@ -7,7 +7,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLD
+from testpaths import GOLD
 
 
 @pytest.fixture(scope="module")
