@@ -86,10 +86,76 @@ def rgemm_blocked(A, B, block=DEFAULT_BLOCK, threads=1):
     return _rgemm(A, B, "blocked")
 
 
+def _mm(A, B):
+    """One blocked real product on the GPU, not counted as a kernel choice."""
+    calls = _kernel_calls["blocked"]
+    C = _rgemm(A, B, "blocked")
+    _kernel_calls["blocked"] = calls
+    return C
+
+
+def _block(M, r0, r1, c0, c1):
+    return RealMatrix(np.ascontiguousarray(M.data[:, r0:r1, c0:c1]))
+
+
+def _strassen(A, B, threshold):
+    """Seven-product recursion on square operands (rgemm.py:116-184): every
+    leaf product and every plane addition runs on the GPU (mpc_rgemm,
+    mpc_mat_add); the recursion itself is host logic.  Odd sizes peel the last
+    row / column (rgemm.py:120-148): each border is one product with the even
+    core plus one outer-product term, the latter formed as an inner-dimension-1
+    product (a zero-initialised chain of length one equals the bare product)."""
+    from .rmatrix import _mat_add
+
+    n, k = A.rows, A.k
+    if n <= threshold:
+        return _mm(A, B)
+    if n % 2:
+        m = n - 1
+        A11, B11 = _block(A, 0, m, 0, m), _block(B, 0, m, 0, m)
+        a12, a21, a22 = _block(A, 0, m, m, n), _block(A, m, n, 0, m), _block(A, m, n, m, n)
+        b12, b21, b22 = _block(B, 0, m, m, n), _block(B, m, n, 0, m), _block(B, m, n, m, n)
+        C = np.empty((k, n, n))
+        C[:, :m, :m] = _mat_add(_strassen(A11, B11, threshold), _mm(a12, b21), 1.0).data
+        C[:, :m, m:] = _mat_add(_mm(A11, b12), _mm(a12, b22), 1.0).data
+        C[:, m:, :m] = _mat_add(_mm(a21, B11), _mm(a22, b21), 1.0).data
+        C[:, m:, m:] = _mat_add(_mm(a21, b12), _mm(a22, b22), 1.0).data
+        return RealMatrix(C)
+    h = n // 2
+    A11, A12, A21, A22 = (_block(A, i * h, i * h + h, j * h, j * h + h) for i in (0, 1) for j in (0, 1))
+    B11, B12, B21, B22 = (_block(B, i * h, i * h + h, j * h, j * h + h) for i in (0, 1) for j in (0, 1))
+    add = lambda X, Y: _mat_add(X, Y, 1.0)   # noqa: E731
+    sub = lambda X, Y: _mat_add(X, Y, -1.0)  # noqa: E731
+    rec = lambda X, Y: _strassen(X, Y, threshold)  # noqa: E731
+    m1 = rec(add(A11, A22), add(B11, B22))
+    m2 = rec(add(A21, A22), B11)
+    m3 = rec(A11, sub(B12, B22))
+    m4 = rec(A22, sub(B21, B11))
+    m5 = rec(add(A11, A12), B22)
+    m6 = rec(sub(A21, A11), add(B11, B12))
+    m7 = rec(sub(A12, A22), add(B21, B22))
+    C = np.empty((k, n, n))
+    C[:, :h, :h] = add(sub(add(m1, m4), m5), m7).data
+    C[:, :h, h:] = add(m3, m5).data
+    C[:, h:, :h] = add(m2, m4).data
+    C[:, h:, h:] = add(add(sub(m1, m2), m3), m6).data
+    return RealMatrix(C)
+
+
 def rgemm_strassen(A, B, threshold=DEFAULT_THRESHOLD, threads=1):
-    """Out of scope: square-only in the reference, so it
-    cannot serve the LU trailing update, and it loses accuracy."""
-    raise NotImplementedError("strassen is outside the B200 hot path (see DESIGN.md)")
+    """Strassen recursion on square operands (rgemm.py:76-91).  Outside the
+    hot path (square-only, so it cannot serve the LU trailing update; SURVEY.md
+    §2): kept for API completeness as a host recursion over the GPU's blocked
+    product and plane additions.  `threads` never changes bits."""
+    _check_mm(A, B)
+    if A.rows != A.cols or B.rows != B.cols:
+        raise ValueError("strassen kernel requires square operands")
+    if threshold < 2:
+        raise ValueError("threshold must be >= 2")
+    check_threads(threads)
+    _check_k(A.k)
+    _kernel_calls["strassen"] += 1
+    return _strassen(A, B, threshold)
 
 
 # ----------------------------------------------------------- complex GEMM
@@ -187,12 +253,27 @@ class PlanarComplexMatrix:
         return f"PlanarComplexMatrix(k={self.k}, shape={self.rows}x{self.cols})"
 
 
+def _cgemm_strassen(A, B, kc, method):
+    """cgemm_3m / cgemm_4m composed from Strassen real products in the
+    reference's order (cmatrix.py:145-169)."""
+    from .rmatrix import _mat_add
+
+    rk = lambda X, Y: rgemm_strassen(X, Y, threshold=kc.threshold, threads=kc.threads)  # noqa: E731
+    if method == "4m":
+        rr, ii = rk(A.re_plane, B.re_plane), rk(A.im_plane, B.im_plane)
+        ir, ri = rk(A.im_plane, B.re_plane), rk(A.re_plane, B.im_plane)
+        return PlanarComplexMatrix(_mat_add(rr, ii, -1.0), _mat_add(ir, ri, 1.0))
+    t1, t2 = rk(A.re_plane, B.re_plane), rk(A.im_plane, B.im_plane)
+    t3 = rk(_mat_add(A.re_plane, A.im_plane, 1.0), _mat_add(B.re_plane, B.im_plane, 1.0))
+    return PlanarComplexMatrix(_mat_add(t1, t2, -1.0), _mat_add(_mat_add(t3, t1, -1.0), t2, -1.0))
+
+
 def _cgemm(A, B, kc, method):
     _check_mm(A.re_plane, B.re_plane)
     kc.validate()
     check_threads(kc.threads)
     if kc.real_kernel == "strassen":
-        raise NotImplementedError("strassen is outside the B200 hot path (see DESIGN.md)")
+        return _cgemm_strassen(A, B, kc, method)
     if not (A.k in VERIFY_K and kc.real_kernel != "ozaki"):
         _check_k(A.k)
     k, m, n = A.re_plane.data.shape

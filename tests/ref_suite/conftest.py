@@ -12,10 +12,10 @@ to build expected values, is outside the hot path; here it is
 served by the CPU oracle (oracle/, itself pinned to the reference), the
 checker -- never by the package.
 
-Skipped (documented): tests of out-of-scope pieces -- Strassen (square-only
-in the reference; its LU variant always fails there), and the
-threads-as-parallelism knobs of the CPU kernels.  Everything else runs as
-written.  All tests here need the GPU (marked gpu)."""
+Nothing is skipped: every test of the four suites runs as written (Strassen
+is a host recursion over the GPU's blocked product and plane additions;
+`threads` is validated and never changes bits).  All tests here need the GPU
+(marked gpu)."""
 
 import os
 import sys
@@ -34,9 +34,7 @@ from paper_2403_16013_b200 import cmatrix, harness, lu, ozaki, rmatrix  # noqa: 
 from paper_2403_16013_b200.rmatrix import Expansion  # noqa: E402
 
 # out-of-scope tests (name substrings) -> reason
-SKIP = {
-    "strassen": "Strassen is outside the B200 hot path (square-only in the reference; DESIGN.md)",
-}
+SKIP = {}
 
 
 def _orc():
