@@ -149,6 +149,16 @@ int mpc_getrs_phases(int k, int method, int64_t n, const double* re, const doubl
                      const int64_t* piv, double* b_re, double* b_im, int phases,
                      void* stream);
 
+/* max_rel_err (lu.py:263-282): max_i |xhat_i - x_i| / |x_i| over complex
+ * moduli in k-component expansion arithmetic, bit for bit the reference's
+ * value (csub, exp_mul / exp_add / exp_div per entry, first strict maximum,
+ * _exp_sqrt's three Newton steps, lu.py:253-260).  Vectors are planar (k, n);
+ * out receives the k components; *zero_index is the first index whose true
+ * component is zero (the reference raises ValueError there) or -1. */
+int mpc_max_rel_err(int k, int64_t n, const double* xhat_re, const double* xhat_im,
+                    const double* x_re, const double* x_im, double* out, int64_t* zero_index,
+                    void* stream);
+
 /* ---- Ozaki scheme (ozaki.py:79-159): the alternative real kernel ---- */
 /* ozaki_split (ozaki.py:79-108) of a (rows x cols) planar operand into d
  * binary64 parts (contiguous (d, rows, cols)) with grid units `scales`

@@ -21,6 +21,7 @@ _SIGS = {
     "mpc_abi_version": (_i, []),
     "mpc_last_error": (ctypes.c_char_p, []),
     "mpc_device_count": (_i, []),
+    "mpc_max_rel_err": (_i, [_i, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "mpc_mat_add": (_i, [_i, _i64, _i64, _p, _i64, _i64, _p, _i64, _i64, _p, _i64, _i64, _d, _p]),
     "mpc_renorm_planes": (_i, [_i, _i64, _i64, _p, _i64, _i64, _p]),
     "mpc_rgemm": (_i, [_i, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _i64, _p, _i64, _i64, _p]),

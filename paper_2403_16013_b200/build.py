@@ -22,7 +22,7 @@ LIBDIR = os.path.join(HERE, "lib")
 OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libmpcb200.so")
 
-SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "inst_k5.cu", "inst_k6.cu", "inst_k8.cu", "abi.cu", "ozaki.cu", "ozaki_tc.cu", "mgpu.cu"]
+SOURCES = ["inst_k2.cu", "inst_k3.cu", "inst_k4.cu", "inst_k5.cu", "inst_k6.cu", "inst_k8.cu", "abi.cu", "ozaki.cu", "ozaki_tc.cu", "mgpu.cu", "metrics.cu"]
 HEADERS = ["expansion.cuh", "kernels.cuh", "ops.h", "prof.h", "sortnet.h", "abi_util.h", "inst_hik.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -49,7 +49,7 @@ def _compile(src, verbose):
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
     if src in ("ozaki.cu", "ozaki_tc.cu"):
         deps.append(os.path.join(CSRC, "ozaki_tc.h"))
-    if src in ("abi.cu", "ozaki.cu", "mgpu.cu"):
+    if src in ("abi.cu", "ozaki.cu", "mgpu.cu", "metrics.cu"):
         deps.append(os.path.join(os.path.dirname(HERE), "include", "mpc_b200.h"))
     if not _stale(obj, deps):
         return obj, ""

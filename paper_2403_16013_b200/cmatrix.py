@@ -60,7 +60,8 @@ def _check_mm(A, B):
 
 def _rgemm(A, B, name):
     _check_mm(A, B)
-    _check_k(A.k)
+    if A.k not in VERIFY_K:  # k = 5, 6, 8: the verification kernels (blocked real GEMM)
+        _check_k(A.k)
     _kernel_calls[name] += 1
     k, m, n = A.data.shape
     l = B.cols

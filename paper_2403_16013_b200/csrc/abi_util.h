@@ -237,17 +237,10 @@ struct WsHolder {
   cudaStream_t st;
   void* mem = nullptr;
   WsHolder(int k, int64_t n, cudaStream_t s) : st(s) {
-    int64_t nb = (n + mpc::PNT - 1) / mpc::PNT + 1;
-    size_t bytes = sizeof(double) * nb * k + sizeof(int64_t) * nb + 64;
     mpc::retain_pool();
-    ck(cudaMallocAsync(&mem, bytes, st), "cudaMallocAsync(ws)");
-    char* b = (char*)mem;
-    ws.status = (int64_t*)b;
-    ws.counter = (unsigned*)(b + 16);
-    ws.prow = (int64_t*)(b + 64);
-    ws.pv = (double*)(b + 64 + sizeof(int64_t) * nb);
-    ck(cudaMemsetAsync(ws.status, 0xFF, sizeof(int64_t), st), "memset status");
-    ck(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), st), "memset counter");
+    ck(cudaMallocAsync(&mem, mpc::panel_ws_bytes(k, n), st), "cudaMallocAsync(ws)");
+    ws = mpc::panel_ws_carve(mem, k, n);
+    ck(mpc::panel_ws_init(ws, st), "memset ws");
   }
   int64_t read_status() {
     int64_t h = -1;

@@ -79,6 +79,10 @@ struct GemmArgs {
   View a, b, c;
   int epi;  // G modes: 0 -> C = P, 1 -> C = C - P (lu.py:157-161 order)
   const int64_t* status;  // LU early-out: skip when *status >= 0
+  // tile queue (nullptr: one tile per CTA, tile = blockIdx.x): persistent CTAs
+  // claim tiles with atomicAdd, so a launch may use fewer CTAs than tiles and
+  // several launches can share one queue (getrf's capped trailing update)
+  unsigned* tile_ctr = nullptr;
 };
 
 MPC_DI void cp_async8(void* smem_ptr, const double* gptr, bool valid) {
@@ -157,7 +161,16 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
   // so one B column panel is reused from L2 by G CTAs in flight
   constexpr int64_t G = MPC_GEMM_RASTER_G;
   const int64_t tiles_m = (g.m + BM - 1) / BM, tiles_n = (g.l + BN - 1) / BN;
-  const int64_t bid = blockIdx.x;
+  __shared__ unsigned next_tile;
+  for (;;) {
+  int64_t bid = blockIdx.x;
+  if (g.tile_ctr != nullptr) {
+    __syncthreads();  // everyone is done with the previous tile's slabs / next_tile
+    if (tid == 0) next_tile = atomicAdd(g.tile_ctr, 1u);
+    __syncthreads();
+    bid = next_tile;
+    if (bid >= tiles_m * tiles_n) return;
+  }
   const int64_t grp = bid / (G * tiles_n);
   const int64_t first_m = grp * G;
   const int64_t gsz = min(tiles_m - first_m, G);
@@ -253,7 +266,11 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
     const double* as = As + st * A_STAGE;
     const double* bs = Bs + st * B_STAGE;
     const int tlen = (int)min((int64_t)BK, g.n - kt * BK);
-#pragma unroll
+    // K >= 3: one copy of the slab body (the renorm networks make it ~4.7k /
+    // ~10k instructions for TD / QD; unrolled over BK the kernel was 0.6 /
+    // 1.3 MB of code and stalled on instruction fetch -- ncu r2:
+    // no_instruction was the top stall reason)
+#pragma unroll(K == 2 ? BK : 1)
     for (int t = 0; t < BK; t++) {
       if (t < tlen) {
         Exp<K> av[NS][TM], bv[NS][TN];
@@ -336,6 +353,8 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
         stexp_<K>(g.c.im + off, g.c.ps, im);
       }
     }
+  if (g.tile_ctr == nullptr) return;
+  }  // tile loop
 }
 
 // ------------------------------------------------------- elementwise
@@ -448,7 +467,39 @@ struct PanelWs {     // device workspace for the pivot reductions
   int64_t* prow;     // [maxblocks]
   unsigned* counter; // last-block detection
   int64_t* status;   // -1 ok, else first singular column
+  unsigned* gbar;    // panel_grid_kernel: [0] barrier arrivals, [1] exits (both 0 between launches)
+  unsigned* tile_ctr;  // getrf: tile queue of the capped trailing update
+  double* slots;     // panel_grid_kernel: [2][PANEL_GRID_GMAX][PANEL_GRID_SLOT] candidates + pivot rows
 };
+
+// Workspace layout (one allocation): a 64-byte header -- status at 0, counter
+// at 16, gbar at 24, tile_ctr at 32 -- then prow, pv and the grid-panel slots.
+constexpr int PANEL_GRID_GMAX = 256;  // CTAs of one panel_grid_kernel launch
+constexpr int PANEL_GRID_SLOT = 40;   // doubles per CTA slot (>= K + 1 + 2 K W)
+inline size_t panel_ws_bytes(int k, int64_t n) {
+  const int64_t nb = (n + 255) / 256 + 1;
+  return 64 + sizeof(int64_t) * nb + sizeof(double) * nb * k +
+         sizeof(double) * 2 * PANEL_GRID_GMAX * PANEL_GRID_SLOT;
+}
+inline PanelWs panel_ws_carve(void* mem, int k, int64_t n) {
+  const int64_t nb = (n + 255) / 256 + 1;
+  char* b = (char*)mem;
+  PanelWs ws;
+  ws.status = (int64_t*)b;
+  ws.counter = (unsigned*)(b + 16);
+  ws.gbar = (unsigned*)(b + 24);
+  ws.tile_ctr = (unsigned*)(b + 32);
+  ws.prow = (int64_t*)(b + 64);
+  ws.pv = (double*)(b + 64 + sizeof(int64_t) * nb);
+  ws.slots = ws.pv + nb * k;
+  return ws;
+}
+// status = -1, counters = 0 (stream ordered)
+inline cudaError_t panel_ws_init(const PanelWs& ws, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(ws.status, 0xFF, sizeof(int64_t), st);
+  if (e != cudaSuccess) return e;
+  return cudaMemsetAsync(ws.counter, 0, 24, st);  // counter, gbar[0..1], tile_ctr
+}
 
 constexpr int PNT = 256;  // threads per block of the panel kernels
 
@@ -745,6 +796,375 @@ __global__ void __launch_bounds__(PanelCluster<K>::NT, 1)
       }
     }
     if (j + 1 < cend) cluster_pick_and_swap<K>(A, j + 1, c0, cend, piv, status, c);
+  }
+}
+
+// ------------------------------------------------- grid-wide base panel
+// The base panel (columns [c0, c0+w), w <= W, rows [c0, n)) in ONE cooperative
+// launch with one row per thread and the row's w columns resident in
+// registers for the whole launch -- the cluster kernel above gives every
+// thread ceil(rows / 4096) rows per column and re-reads them from memory.
+//
+// Row interchanges are virtual: every thread carries the current position
+// `pos` of its row (_swap_rows, _kernels.py:597-608, exchanges positions jj
+// and p -- here the two owning threads exchange their `pos`), the thread whose
+// row becomes the pivot row retires, and the rows are written to their final
+// positions at the end.  The candidate order (|Re| + |Im|, ties to the lower
+// CURRENT position) is the reference's.
+//
+// Per column ONE grid barrier: every CTA reduces its candidates, the owning
+// thread publishes (value, position, the row's values) to the CTA's slot and
+// arrives; after the barrier warp 0 of every CTA reduces the slots -- the
+// comparator is a total preorder, so every CTA picks the same row -- and
+// stages the pivot row in shared memory.  Only l = cdiv(a, pivot) and the
+// update of the NEXT column sit on the critical path: the updates of the
+// remaining columns run after the next arrival, under the barrier latency.
+// Element operation sequences are those of panel_step_kernel.
+template <int K>
+struct PanelGrid {
+  static constexpr int NT = 256;
+  static constexpr int W = K == 2 ? 8 : 4;
+  static_assert(K + 1 + 2 * K * W <= PANEL_GRID_SLOT, "slot too small");
+};
+
+MPC_DI unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// cand_better on (value, position) pairs.  DD: candidates are dd_add outputs,
+// i.e. normalized (hi = fl(hi + lo)), whose representation is unique, so
+// different leading limbs already order the exact values; equal leading
+// limbs (and k >= 3) take the reference's exact test.
+template <int K>
+MPC_DI bool cand_better_f(const Exp<K>& av, int64_t ar, const Exp<K>& bv, int64_t br) {
+  if (ar < 0) return false;
+  if (br < 0) return true;
+  if constexpr (K == 2) {
+    if (av.c[0] != bv.c[0]) return av.c[0] > bv.c[0];
+  }
+  Exp<K> d = exp_sub(av, bv);
+  if (d.c[0] > 0.0) return true;
+  if (d.c[0] < 0.0) return false;
+  return ar < br;
+}
+
+// TPR = 2: two adjacent lanes share a row (same values, same operations)
+// and split l = cdiv(a, pivot) -- the longest dependent chain of a column
+// step -- between them: lane 0 forms Re l = (ar br + ai bi) / d, lane 1
+// Im l = (ai br - ar bi) / d (cdiv_core, _kernels.py:549-561; exp_sub(x, y) is
+// exp_add(x, -y), so both lanes run one instruction stream), exchanged by
+// shuffle.  Only lane 0 of a row competes for the pivot and stores.
+template <int K, int TPR>
+__global__ void __launch_bounds__(PanelGrid<K>::NT, 1)
+    panel_grid_kernel(View A, int64_t n, int64_t c0, int w, int use3m, int64_t* piv,
+                      int64_t* status, unsigned* gbar, double* slots) {
+  using PG = PanelGrid<K>;
+  constexpr int NT = PG::NT, W = PG::W, NW = NT / 32, SLOT = PANEL_GRID_SLOT;
+  constexpr int ROWS = NT / TPR;
+  __shared__ double ubuf[2][2 * K * W];  // pivot row: [Re limbs][W], [Im limbs][W]
+  __shared__ int64_t pick_s[2];
+  __shared__ double red_v[NW][K];
+  __shared__ int64_t red_r[NW];
+  __shared__ int red_t[NW];
+  __shared__ double win_v[K];
+  __shared__ int64_t win_r;
+  __shared__ int win_tid;
+
+  if (*(volatile int64_t*)status >= 0) return;  // uniform: written only by earlier launches
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned G = gridDim.x;
+  const int sub = tid % TPR;  // lane within the row's group
+  const int64_t home = c0 + (int64_t)blockIdx.x * ROWS + tid / TPR;
+  const bool valid = home < n;
+  int64_t pos = home;
+  bool active = valid;
+  Exp<K> xr[W], xi[W];
+#pragma unroll
+  for (int i = 0; i < W; i++) {
+    if (valid && i < w) {
+      xr[i] = ldexp_<K>(A.re + home * A.ld + c0 + i, A.ps);
+      xi[i] = ldexp_<K>(A.im + home * A.ld + c0 + i, A.ps);
+    } else {
+      xr[i] = exp_zero<K>();
+      xi[i] = exp_zero<K>();
+    }
+  }
+  unsigned epoch = 0;
+  bool singular = false;
+  for (int q = 0; q < w; q++) {
+    const int par = q & 1;
+    const int64_t jj = c0 + q;
+    // 1. this row's candidate for column q
+    Exp<K> cv = exp_zero<K>();
+    int64_t crow = -1;
+    int ctid = tid;
+    if (active && sub == 0) {
+      Exp<K> ar = exp_zero<K>(), ai = exp_zero<K>();
+#pragma unroll
+      for (int i = 0; i < W; i++)
+        if (i == q) {
+          ar = xr[i];
+          ai = xi[i];
+        }
+      cv = exp_add(exp_abs(ar), exp_abs(ai));
+      crow = exp_greater(cv, exp_zero<K>()) ? pos : -1;
+    }
+    // 2. CTA argmax, carrying the owning thread
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      Exp<K> ov;
+#pragma unroll
+      for (int c = 0; c < K; c++) ov.c[c] = __shfl_down_sync(0xffffffffu, cv.c[c], off);
+      const int64_t orow = __shfl_down_sync(0xffffffffu, crow, off);
+      const int otid = __shfl_down_sync(0xffffffffu, ctid, off);
+      if (cand_better_f<K>(ov, orow, cv, crow)) {
+        cv = ov;
+        crow = orow;
+        ctid = otid;
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < K; c++) red_v[wid][c] = cv.c[c];
+      red_r[wid] = crow;
+      red_t[wid] = ctid;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      if (lane < NW) {
+#pragma unroll
+        for (int c = 0; c < K; c++) cv.c[c] = red_v[lane][c];
+        crow = red_r[lane];
+        ctid = red_t[lane];
+      } else {
+        crow = -1;
+      }
+#pragma unroll
+      for (int off = NW / 2; off > 0; off >>= 1) {
+        Exp<K> ov;
+#pragma unroll
+        for (int c = 0; c < K; c++) ov.c[c] = __shfl_down_sync(0xffffffffu, cv.c[c], off);
+        const int64_t orow = __shfl_down_sync(0xffffffffu, crow, off);
+        const int otid = __shfl_down_sync(0xffffffffu, ctid, off);
+        if (cand_better_f<K>(ov, orow, cv, crow)) {
+          cv = ov;
+          crow = orow;
+          ctid = otid;
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < K; c++) win_v[c] = cv.c[c];
+        win_r = crow;
+        win_tid = crow >= 0 ? ctid : 0;
+      }
+    }
+    __syncthreads();
+    // the previous column's deferred updates (columns > q): l = x[q-1], u =
+    // the previous pivot row.  The CTA's candidate row runs them before it is
+    // published (its values become U's row), every other row under the barrier
+    auto deferred = [&]() {
+      Exp<K> lr = exp_zero<K>(), li = exp_zero<K>();
+#pragma unroll
+      for (int i = 0; i < W; i++)
+        if (i == q - 1) {
+          lr = xr[i];
+          li = xi[i];
+        }
+      const double* ub = &ubuf[par ^ 1][0];
+#pragma unroll
+      for (int i = 2; i < W; i++)
+        if (i > q && i < w) {
+          Exp<K> ur, ui;
+#pragma unroll
+          for (int c = 0; c < K; c++) {
+            ur.c[c] = ub[c * W + i];
+            ui.c[c] = ub[(K + c) * W + i];
+          }
+          Cx<K> pr = cmul(use3m != 0, lr, li, ur, ui);
+          xr[i] = exp_sub(xr[i], pr.re);
+          xi[i] = exp_sub(xi[i], pr.im);
+        }
+    };
+    const bool is_pub = tid == win_tid;
+    if (is_pub) {  // publish the CTA's candidate and its row, then arrive
+      if (q > 0 && active) deferred();
+      double* sl = slots + ((size_t)par * PANEL_GRID_GMAX + blockIdx.x) * SLOT;
+      const int64_t wr = win_r;
+      if (G > 1) {
+#pragma unroll
+        for (int c = 0; c < K; c++) sl[c] = win_v[c];
+        sl[K] = __longlong_as_double(wr);
+      }
+      if (wr >= 0) {
+        double* dst = G > 1 ? sl + K + 1 : &ubuf[par][0];
+#pragma unroll
+        for (int i = 0; i < W; i++)
+#pragma unroll
+          for (int c = 0; c < K; c++) {
+            dst[c * W + i] = xr[i].c[c];
+            dst[(K + c) * W + i] = xi[i].c[c];
+          }
+      }
+      if (G > 1) {
+        __threadfence();
+        atomicAdd(&gbar[0], 1u);
+      } else {
+        pick_s[par] = wr;
+      }
+    }
+    // 3. the other rows' deferred updates, under the barrier
+    if (q > 0 && active && !is_pub) deferred();
+    // 4. every CTA's candidate is published
+    if (G > 1) {
+      epoch++;
+      if (tid == 0)
+        while (ld_acquire_u32(&gbar[0]) < epoch * G) {
+        }
+      __syncthreads();
+      // 5. warp 0: the global argmax (same result in every CTA), pivot row to smem
+      if (wid == 0) {
+        Exp<K> bv = exp_zero<K>();
+        int64_t brow = -1;
+        unsigned bb = 0;
+        for (unsigned b = lane; b < G; b += 32) {
+          const double* sl = slots + ((size_t)par * PANEL_GRID_GMAX + b) * SLOT;
+          Exp<K> ov;
+#pragma unroll
+          for (int c = 0; c < K; c++) ov.c[c] = __ldcg(sl + c);
+          const int64_t orow = __double_as_longlong(__ldcg(sl + K));
+          if (cand_better_f<K>(ov, orow, bv, brow)) {
+            bv = ov;
+            brow = orow;
+            bb = b;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          Exp<K> ov;
+#pragma unroll
+          for (int c = 0; c < K; c++) ov.c[c] = __shfl_down_sync(0xffffffffu, bv.c[c], off);
+          const int64_t orow = __shfl_down_sync(0xffffffffu, brow, off);
+          const unsigned ob = __shfl_down_sync(0xffffffffu, bb, off);
+          if (cand_better_f<K>(ov, orow, bv, brow)) {
+            bv = ov;
+            brow = orow;
+            bb = ob;
+          }
+        }
+        brow = __shfl_sync(0xffffffffu, brow, 0);
+        bb = __shfl_sync(0xffffffffu, bb, 0);
+        if (brow >= 0) {
+          const double* sl = slots + ((size_t)par * PANEL_GRID_GMAX + bb) * SLOT + K + 1;
+          for (int e = lane; e < 2 * K * W; e += 32) ubuf[par][e] = __ldcg(sl + e);
+        }
+        if (lane == 0) pick_s[par] = brow;
+      }
+    }
+    __syncthreads();
+    const int64_t P = pick_s[par];
+    if (P < 0) {  // lu_panel returns jj (_kernels.py:622-624); uniform across the grid
+      if (blockIdx.x == 0 && tid == 0 && *status < 0) *status = jj;
+      singular = true;
+      break;
+    }
+    if (blockIdx.x == 0 && tid == 0) piv[jj] = P;
+    if (active) {
+      if (pos == P) {
+        pos = jj;
+        active = false;  // this row is U's row jj now
+      } else if (pos == jj) {
+        pos = P;
+      }
+    }
+    Cx<K> l;
+    if constexpr (TPR == 2) {
+      Exp<K> quo = exp_zero<K>();
+      if (active) {
+        Exp<K> ar = exp_zero<K>(), ai = exp_zero<K>(), br, bi;
+#pragma unroll
+        for (int i = 0; i < W; i++)
+          if (i == q) {
+            ar = xr[i];
+            ai = xi[i];
+          }
+        const double* ub = &ubuf[par][0];
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+          br.c[c] = ub[c * W + q];
+          bi.c[c] = ub[(K + c) * W + q];
+        }
+        const Exp<K> d = exp_add(exp_mul(br, br), exp_mul(bi, bi));
+        const Exp<K> t1 = exp_mul(sub ? ai : ar, br);
+        Exp<K> t2 = exp_mul(sub ? ar : ai, bi);
+        if (sub) t2 = exp_neg(t2);
+        quo = exp_div(exp_add(t1, t2), d);
+      }
+      Exp<K> oth;  // the partner lane's quotient (every lane takes part)
+#pragma unroll
+      for (int c = 0; c < K; c++) oth.c[c] = __shfl_xor_sync(0xffffffffu, quo.c[c], 1);
+      l.re = sub ? oth : quo;
+      l.im = sub ? quo : oth;
+    }
+    if (active) {
+      const double* ub = &ubuf[par][0];
+      if constexpr (TPR == 1) {
+        Exp<K> ar = exp_zero<K>(), ai = exp_zero<K>(), br, bi;
+#pragma unroll
+        for (int i = 0; i < W; i++)
+          if (i == q) {
+            ar = xr[i];
+            ai = xi[i];
+          }
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+          br.c[c] = ub[c * W + q];
+          bi.c[c] = ub[(K + c) * W + q];
+        }
+        l = cdiv(ar, ai, br, bi);
+      }
+#pragma unroll
+      for (int i = 0; i < W; i++)
+        if (i == q) {
+          xr[i] = l.re;
+          xi[i] = l.im;
+        }
+      if (q + 1 < w) {  // the next column first: its candidates gate the next barrier
+        Exp<K> ur, ui;
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+          ur.c[c] = ub[c * W + q + 1];
+          ui.c[c] = ub[(K + c) * W + q + 1];
+        }
+        Cx<K> pr = cmul(use3m != 0, l.re, l.im, ur, ui);
+#pragma unroll
+        for (int i = 1; i < W; i++)
+          if (i == q + 1) {
+            xr[i] = exp_sub(xr[i], pr.re);
+            xi[i] = exp_sub(xi[i], pr.im);
+          }
+      }
+    }
+  }
+  (void)singular;
+  // rows to their final positions (every CTA loaded its rows before its first
+  // arrival, so no row is overwritten before its owner has read it)
+  if (valid && sub == 0) {
+#pragma unroll
+    for (int i = 0; i < W; i++)
+      if (i < w) {
+        stexp_<K>(A.re + pos * A.ld + c0 + i, A.ps, xr[i]);
+        stexp_<K>(A.im + pos * A.ld + c0 + i, A.ps, xi[i]);
+      }
+  }
+  if (G > 1 && tid == 0) {  // the last CTA out re-arms the barrier words
+    __threadfence();
+    if (atomicAdd(&gbar[1], 1u) == G - 1) {
+      gbar[0] = 0u;
+      gbar[1] = 0u;
+    }
   }
 }
 
@@ -1098,12 +1518,16 @@ inline void retain_pool() {
 // released on every exit path (a failed launch throws LaunchError mid-loop).
 struct SideStream {
   cudaStream_t sp = nullptr;
-  cudaEvent_t ev_narrow = nullptr, ev_panel = nullptr;
+  cudaStream_t sh = nullptr;  // helper launches of the capped trailing update
+  cudaEvent_t ev_narrow = nullptr, ev_panel = nullptr, ev_queue = nullptr, ev_helper = nullptr;
   SideStream() {
     int lo = 0, hi = 0;
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_queue, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_helper, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming) != cudaSuccess) {
       release();
       throw LaunchError{"side stream / event creation"};
@@ -1115,9 +1539,12 @@ struct SideStream {
   void release() {
     if (ev_panel) cudaEventDestroy(ev_panel);
     if (ev_narrow) cudaEventDestroy(ev_narrow);
+    if (ev_queue) cudaEventDestroy(ev_queue);
+    if (ev_helper) cudaEventDestroy(ev_helper);
     if (sp) cudaStreamDestroy(sp);
-    sp = nullptr;
-    ev_narrow = ev_panel = nullptr;
+    if (sh) cudaStreamDestroy(sh);
+    sp = sh = nullptr;
+    ev_narrow = ev_panel = ev_queue = ev_helper = nullptr;
   }
 };
 
@@ -1158,16 +1585,20 @@ struct Ops {
   static constexpr int TN = (K == 2) ? 2 : 1;
 
   template <int MODE, int BM_, int BN_, int BK_, int TM_, int TN_, int MINB_>
-  static void launch_cfg(const GemmArgs& g, cudaStream_t st, int cls, double ops) {
+  static void launch_cfg(const GemmArgs& g, cudaStream_t st, int cls, double ops, int ctas = 0) {
     using Cfg = GemmCfg<K, MODE, BM_, BN_, BK_, TM_, TN_>;
     auto kern = gemm_kernel<K, MODE, BM_, BN_, BK_, TM_, TN_, MINB_>;
     static unsigned long long attr_set = 0;
     if (first_on_device(attr_set))
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    dim3 grid((unsigned)((int64_t)cdiv_u(g.l, BN_) * (int64_t)cdiv_u(g.m, BM_)));
-    int tok_ = prof_begin(cls, ops, st);
+    int64_t tiles = (int64_t)cdiv_u(g.l, BN_) * (int64_t)cdiv_u(g.m, BM_);
+    if (g.tile_ctr != nullptr) tiles = std::min<int64_t>(tiles, std::max(ctas, 1));  // persistent CTAs
+    dim3 grid((unsigned)tiles);
+    // a helper launch on a shared queue (ops < 0) is not timed: it runs inside
+    // the main launch's interval, which already carries the work
+    int tok_ = ops >= 0.0 ? prof_begin(cls, ops, st) : -1;
     kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(g);
-    prof_end(tok_, st);
+    if (ops >= 0.0) prof_end(tok_, st);
     check_launch("gemm_kernel");
   }
 
@@ -1225,6 +1656,28 @@ struct Ops {
       gemm_launch<MODE_G3>(g, st, PC_GEMM, 3 * OpModel<K>::real_mac);
     else
       gemm_launch<MODE_G4>(g, st, PC_GEMM, 4 * OpModel<K>::real_mac);
+  }
+
+  // The same product computed by `ctas` persistent CTAs that claim tiles from
+  // the queue `ctr` (zeroed by the caller, stream ordered).  Several launches
+  // may share one queue: getrf caps the trailing update while the next panel
+  // is being factored and adds the remaining CTAs once it is done.  Tiles are
+  // the full-size configuration's, so every element's chain is unchanged.
+  // helper = true: not timed / counted as work (it runs inside the main
+  // launch's interval).
+  static void cgemm_queued(bool use3m, int64_t m, int64_t n, int64_t l, View a, View b, View c,
+                           int epi, cudaStream_t st, const int64_t* status, unsigned* ctr, int ctas,
+                           bool helper) {
+    if (m <= 0 || l <= 0) return;
+    GemmArgs g{m, n, l, a, b, c, epi, status};
+    g.tile_ctr = ctr;
+    const double ops = helper ? -1.0
+                              : (double)m * (double)l * (double)n * (use3m ? 3.0 : 4.0) *
+                                    OpModel<K>::real_mac;
+    if (use3m)
+      launch_cfg<MODE_G3, BM, BN, BK, TM, TN, 2>(g, st, PC_GEMM, ops, ctas);
+    else
+      launch_cfg<MODE_G4, BM, BN, BK, TM, TN, 2>(g, st, PC_GEMM, ops, ctas);
   }
 
   // chained update C -= L (x) U, each element's subtractions in column order
@@ -1330,9 +1783,54 @@ struct Ops {
     return cs;
   }
 
+  // CTAs of panel_grid_kernel that can be co-resident (0: use the cluster /
+  // per-column kernels -- MPC_PANEL=cluster or =launches, or no cooperative
+  // launch support)
+  static int panel_grid_max() {
+    static int g = [] {
+      const char* e = getenv("MPC_PANEL");
+      if (e && (std::string(e) == "launches" || std::string(e) == "cluster")) return 0;
+      int dev = 0, coop = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+      if (!coop) return 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, panel_grid_kernel<K, 2>,
+                                                        PanelGrid<K>::NT, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+      return (int)std::min<int64_t>(PANEL_GRID_GMAX, per_sm * sm_count());
+    }();
+    return g;
+  }
+
   static void panel_base(bool use3m, View A, int64_t n, int64_t c0, int64_t w, int64_t* piv,
                          PanelWs ws, cudaStream_t st) {
     int64_t cend = c0 + w;
+    // one row per thread, rows resident in registers: a cooperative grid
+    if (const int gmax = panel_grid_max()) {
+      // two lanes per row (split cdiv) while the grid fits, else one
+      static const int tpr_max = [] {
+        const char* e = getenv("MPC_PANEL_TPR");
+        return e && atoi(e) == 1 ? 1 : 2;
+      }();
+      constexpr int NT = PanelGrid<K>::NT;
+      const int tpr = (tpr_max == 2 && (n - c0 + NT / 2 - 1) / (NT / 2) <= gmax) ? 2 : 1;
+      const int64_t G = (n - c0 + NT / tpr - 1) / (NT / tpr);
+      if (G <= gmax && w <= PanelGrid<K>::W) {
+        int wi = (int)w, u3 = use3m ? 1 : 0;
+        void* args[] = {&A, &n, &c0, &wi, &u3, &piv, &ws.status, &ws.gbar, &ws.slots};
+        double ops = 0.0;
+        for (int64_t j = c0; j < cend; j++) ops += (double)(n - j - 1) * (double)(cend - j - 1);
+        int tok_ = prof_begin(PC_PANEL, ops * OpModel<K>::upd(use3m), st);
+        cudaLaunchCooperativeKernel(
+            tpr == 2 ? (void*)panel_grid_kernel<K, 2> : (void*)panel_grid_kernel<K, 1>,
+            dim3((unsigned)G), dim3(NT), args, 0, st);
+        prof_end(tok_, st);
+        check_launch("panel_grid_kernel");
+        return;
+      }
+    }
     if (int csmax = panel_cluster_size()) {
       static unsigned long long attr = 0;
       if (first_on_device(attr))
@@ -1420,6 +1918,16 @@ struct Ops {
           status);
   }
 
+  // CTAs of the trailing update's first (capped) launch while the next panel
+  // is factored beside it (MPC_GEMM_CAP; 0 = one uncapped launch)
+  static int gemm_cap() {
+    static int c = [] {
+      const char* e = getenv("MPC_GEMM_CAP");
+      return e ? atoi(e) : 0;
+    }();
+    return c;
+  }
+
   // lu._factor (lu.py:129-163) with depth-1 lookahead: while `st` applies
   // panel b's trailing update to columns right of block b+1, panel b+1
   // (already updated by b) is factored on a high-priority side stream.
@@ -1440,6 +1948,7 @@ struct Ops {
       cudaEventRecord(e, s);
       tev.push_back(e);
     };
+    bool helper_pending = false;
     const ColSource src = col_source();
     auto need = [&](int64_t c1) {
       if (src.need) src.need(src.ctx, std::min(c1, n), st);
@@ -1475,12 +1984,39 @@ struct Ops {
           need(c0 + ch);
           update_cols(use3m, A, n, jb, kw, c0, std::min(n, c0 + ch), piv, ws.status, st);
         }
+      } else if (gemm_cap() > 0 && end + kw2 < n) {
+        // capped trailing update: `cap` persistent CTAs claim tiles from a
+        // queue, leaving room on every SM for the panel's kernels (which
+        // otherwise wait for whole 0.4 - 0.8 ms GEMM CTAs to retire before
+        // each of their ~300 dependent launches); once the panel is done a
+        // helper launch on the same queue restores full occupancy
+        const int64_t c0 = end + kw2;
+        const int full = 2 * (int)sm_count();
+        const int cap = std::min(gemm_cap(), full);
+        laswp(A, c0, n - c0, piv, jb, end, st, ws.status);
+        trsm(use3m, kw, n - c0, A.sub(jb, jb), A.sub(jb, c0), st, ws.status);
+        cudaMemsetAsync(ws.tile_ctr, 0, sizeof(unsigned), st);
+        cudaEventRecord(ss.ev_queue, st);
+        cgemm_queued(use3m, n - end, kw, n - c0, A.sub(end, jb), A.sub(jb, c0), A.sub(end, c0), 1,
+                     st, ws.status, ws.tile_ctr, cap, false);
+        if (cap < full) {
+          cudaStreamWaitEvent(ss.sh, ss.ev_queue, 0);
+          cudaStreamWaitEvent(ss.sh, ev_panel, 0);
+          cgemm_queued(use3m, n - end, kw, n - c0, A.sub(end, jb), A.sub(jb, c0), A.sub(end, c0),
+                       1, ss.sh, ws.status, ws.tile_ctr, full - cap, true);
+          cudaEventRecord(ss.ev_helper, ss.sh);
+          helper_pending = true;
+        }
       } else {
         update_cols(use3m, A, n, jb, kw, end + kw2, n, piv, ws.status, st);
       }
       if (row_sink().fn) row_sink().fn(row_sink().ctx, jb, end, st);
       mark(st);
       cudaStreamWaitEvent(st, ev_panel, 0);
+      if (helper_pending) {
+        cudaStreamWaitEvent(st, ss.ev_helper, 0);
+        helper_pending = false;
+      }
       mark(st);
     }
     if (trace) {

@@ -180,16 +180,10 @@ int64_t mpc_getrf_ngpu(int k, int method, int64_t n, int64_t K, double* re, doub
       rk->pan_im[s] = (double*)dmalloc(pan);
     }
     rk->piv = (int64_t*)dmalloc(sizeof(int64_t) * n);
-    int64_t wb = (n + mpc::PNT - 1) / mpc::PNT + 1;
-    rk->wsmem = dmalloc(sizeof(double) * wb * k + sizeof(int64_t) * wb + 64);
-    char* w = (char*)rk->wsmem;
-    rk->ws.status = (int64_t*)w;
-    rk->ws.counter = (unsigned*)(w + 16);
-    rk->ws.prow = (int64_t*)(w + 64);
-    rk->ws.pv = (double*)(w + 64 + sizeof(int64_t) * wb);
+    rk->wsmem = dmalloc(mpc::panel_ws_bytes(k, n));
+    rk->ws = mpc::panel_ws_carve(rk->wsmem, k, n);
     ck(cudaStreamWaitEvent(rk->st, ev_in, 0), "cudaStreamWaitEvent");
-    ck(cudaMemsetAsync(rk->ws.status, 0xFF, sizeof(int64_t), rk->st), "memset status");
-    ck(cudaMemsetAsync(rk->ws.counter, 0, sizeof(unsigned), rk->st), "memset counter");
+    ck(mpc::panel_ws_init(rk->ws, rk->st), "memset ws");
     iota_kernel_mg<<<(unsigned)((n + 255) / 256), 256, 0, rk->st>>>(rk->piv, n);
     ck(cudaGetLastError(), "iota");
     // scatter: this rank's block columns, every limb plane (H2D, or peer /

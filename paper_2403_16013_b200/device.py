@@ -87,7 +87,8 @@ def accuracy(a_re, a_im, f_re, f_im, piv, method="3m", seed=0):
 
     * forward error: b = A x_true with x_true = 1 + 1i (the DD 4M product,
       BASELINE configs 0 / 2 / 4), x = getrs(b), max_i |x_i - x_true_i| /
-      |x_true_i| in binary64 from the limb-wise difference (lu.max_rel_err);
+      |x_true_i| in binary64 from the limb-wise difference (lu.max_rel_err gives
+      the reference's expansion-arithmetic value of the same metric);
     * backward error: lu.backward_error_probe on the device -- r = P A v -
       L (U v) at k + 2 components for a seeded v, ||r|| / (||A|| ||v||) in
       the infinity norm of |Re| + |Im| moduli (a lower bound of the

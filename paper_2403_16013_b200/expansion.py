@@ -17,3 +17,24 @@ def eps_for(k):
 
 def digits_for(k):
     return int(math.floor(53 * k * math.log10(2.0)))
+
+
+def exp_to_string(x, digits=None):
+    """Decimal string of an expansion's exact value, correctly rounded to
+    `digits` significant digits (expansion.py:199-215; default: the digits k
+    components carry).  `x` is anything with .components / .k / .to_fraction()
+    (rmatrix.Expansion)."""
+    from decimal import Decimal, localcontext
+
+    if digits is None:
+        digits = digits_for(x.k)
+    f = x.to_fraction()
+    if f == 0:
+        return "0.0"
+    with localcontext() as ctx:
+        ctx.prec = digits
+        d = Decimal(f.numerator) / Decimal(f.denominator)
+    s = str(d)
+    if "E" in s:
+        return s.replace("E", "e")
+    return s if "." in s else s + ".0"

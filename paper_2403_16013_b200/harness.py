@@ -37,7 +37,7 @@ import numpy as np
 
 from . import _lib
 from .cmatrix import DEFAULT_SPLITS, KernelChoice, PlanarComplexMatrix, cgemm_4m
-from .expansion import PRECISIONS, REFERENCE_K, eps_for
+from .expansion import PRECISIONS, REFERENCE_K, eps_for, exp_to_string
 from .lu import (ComplexVector, LinearSystem, SingularMatrixError, backward_error_probe,
                  lu_blocked, lu_normal, max_rel_err, reconstruction_error, solve)
 from .rmatrix import RealMatrix, mat_sub
@@ -300,7 +300,7 @@ def run_bench(cfg):
                               run_id=_run_id(cfg, K, t))
             if status == "ok":
                 med = rec.rep_median_seconds
-                rec.max_relerr = float_to_string(float(max_rel_err(xhat, x_true)), 17)
+                rec.max_relerr = exp_to_string(max_rel_err(xhat, x_true), 17)
                 rec.gflops_conv = 8.0 * cfg.n ** 3 / 3.0 / med / 1e9
                 if cfg.kernel != "ozaki":
                     ops = _factor_ops(cfg.n, K, k, cfg.method, cfg.algorithm == "normal")

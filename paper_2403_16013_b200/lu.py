@@ -83,6 +83,17 @@ class ComplexVector:
     def zeros(cls, n, k):
         return cls(np.zeros((k, n)), np.zeros((k, n)))
 
+    @classmethod
+    def from_scalars(cls, zs):
+        """One entry per ComplexScalar (lu.py:63-69)."""
+        zs = list(zs)
+        if not zs:
+            raise ValueError("from_scalars needs at least one scalar")
+        v = cls.zeros(len(zs), zs[0].re.k)
+        for i, z in enumerate(zs):
+            v.set_at(i, z)
+        return v
+
     def copy(self):
         return ComplexVector(self.re.copy(), self.im.copy())
 
@@ -308,26 +319,24 @@ def permuted(A, pivots):
 
 
 def max_rel_err(xhat, x):
-    """max_i |xhat_i - x_i| / |x_i| over complex moduli (lu.py:263-282).
-
-    Returned as a float: the difference is formed limb-wise in binary64
-    (the leading-limb difference is exact for nearby values), which is ample
-    for an error *metric*; the reference carries it as an expansion."""
+    """max_i |xhat_i - x_i| / |x_i| over complex moduli (lu.py:263-282), on
+    the GPU in the reference's expansion arithmetic: the returned Expansion
+    is the reference's value bit for bit (mpc_max_rel_err)."""
     if xhat.n != x.n or xhat.k != x.k:
         raise ValueError("vectors must share length and component count")
-
-    def diff(a, b):
-        d = np.zeros(a.shape[1])
-        for c in range(a.shape[0] - 1, -1, -1):
-            d += a[c] - b[c]
-        return d
-
-    dr, di = diff(xhat.re, x.re), diff(xhat.im, x.im)
-    xr, xi = x.re.sum(axis=0), x.im.sum(axis=0)
-    den = np.hypot(xr, xi)
-    if np.any(den == 0.0):
-        raise ValueError(f"zero true component at index {int(np.argmax(den == 0.0))}")
-    return float(np.max(np.hypot(dr, di) / den)) if x.n else 0.0
+    k, n = x.k, x.n
+    out = np.zeros(k)
+    if n == 0:
+        return Expansion(out)
+    if k not in (2, 3, 4):
+        raise ValueError(f"component count k={k} not supported on the B200 path (2, 3 or 4)")
+    zero = np.full(1, -1, dtype=np.int64)
+    _lib.check(_lib.lib().mpc_max_rel_err(k, n, _lib.ptr(xhat.re), _lib.ptr(xhat.im),
+                                          _lib.ptr(x.re), _lib.ptr(x.im), _lib.ptr(out),
+                                          _lib.ptr(zero), None), "max_rel_err")
+    if zero[0] >= 0:
+        raise ValueError(f"zero true component at index {int(zero[0])}")
+    return Expansion(out)
 
 
 def _check_inplace_args(re, im, piv):

@@ -370,3 +370,39 @@ def test_cfg3_lu_digest(k):
         f = mp.lu_blocked(pc(re, im), c["K"], kc=mp.KernelChoice(method=c["method"]))
         assert [int(p) for p in f.pivots] == c["pivots"], c["method"]
         assert digest(f.packed.re_plane.data, f.packed.im_plane.data) == c["digest"], c["method"]
+
+
+# ------------------------------------------------ Strassen (API completeness)
+
+def test_golden_strassen():
+    """rgemm_strassen and cgemm(real_kernel="strassen") against the unmodified
+    reference's outputs (oracle/gen_golden_strassen.py): even, odd (peeled)
+    and mixed recursion depths, k = 2, 3, 4 -- bit for bit."""
+    g = np.load(os.path.join(GOLD, "strassen.npz"))
+    keys = sorted({k[:-2] for k in g.files if k.startswith("r_")})
+    assert len(keys) == 7
+    for key in keys:
+        thr = int(key.rsplit("_t", 1)[1])
+        C = mp.rgemm_strassen(mp.RealMatrix(g[key + "_a"]), mp.RealMatrix(g[key + "_b"]), threshold=thr)
+        assert beq(C.data, g[key + "_c"]), (key, first_diff(C.data, g[key + "_c"]))
+    for meth in ("3m", "4m"):
+        key = f"c_{meth}_k2_n14_t4"
+        A, B = pc(g[key + "_are"], g[key + "_aim"]), pc(g[key + "_bre"], g[key + "_bim"])
+        C = mp.cgemm(A, B, mp.KernelChoice(method=meth, real_kernel="strassen", threshold=4))
+        assert beq(C.re_plane.data, g[key + "_cre"]) and beq(C.im_plane.data, g[key + "_cim"]), key
+
+
+def test_golden_max_rel_err():
+    """lu.max_rel_err (mpc_max_rel_err) against the unmodified reference's
+    expansion-valued result (oracle/gen_golden_metrics.py), bit for bit."""
+    g = np.load(os.path.join(GOLD, "metrics.npz"))
+    keys = sorted({k.rsplit("_", 1)[0] for k in g.files})
+    assert len(keys) == 12
+    for key in keys:
+        e = mp.max_rel_err(mp.ComplexVector(g[key + "_hr"], g[key + "_hi"]),
+                           mp.ComplexVector(g[key + "_xr"], g[key + "_xi"]))
+        assert beq(e.components, g[key + "_err"]), (key, e.components, g[key + "_err"])
+    x = mp.ComplexVector.zeros(3, 2)
+    x.re[0] = [1.0, 0.0, 2.0]
+    with pytest.raises(ValueError, match="zero true component at index 1"):
+        mp.max_rel_err(x, x)
