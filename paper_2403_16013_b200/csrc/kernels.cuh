@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstdio>
 #include <string>
@@ -272,7 +273,23 @@ __global__ void __launch_bounds__(GemmCfg<K, MODE, BM, BN, BK, TM, TN>::NT, MINB
     // no_instruction was the top stall reason)
 #pragma unroll(K == 2 ? BK : 1)
     for (int t = 0; t < BK; t++) {
-      if (t < tlen) {
+      if constexpr (K >= 3 && K <= 4 && TM == 1 && TN == 1 && !MI::CHAINED) {
+        // TD / QD: ONE copy of exp_mul + exp_add, looped over the NACC chains
+        // (operands picked from shared memory by slot, accumulators indexed
+        // at run time, i.e. L1-resident local memory): a third / a quarter of
+        // the code again, so the slab body stays in the instruction cache
+        if (t < tlen) {
+#pragma unroll 1
+          for (int q = 0; q < NACC; q++) {
+            // G3: (re, re) (im, im) (sum, sum); G4: rr, ii, ir, ri; REAL: slot 0
+            const int sa = MODE == MODE_G4 ? ((q == 1 || q == 2) ? 1 : 0) : q;
+            const int sb = MODE == MODE_G4 ? ((q == 1 || q == 3) ? 1 : 0) : q;
+            const Exp<K> a = lds_exp<K>(as + ((sa * BM + ty) * BK + t) * K);
+            const Exp<K> b = lds_exp<K>(bs + ((sb * BK + t) * BN + tx) * K);
+            acc[0][0][q] = exp_add(acc[0][0][q], exp_mul(a, b));
+          }
+        }
+      } else if (t < tlen) {
         Exp<K> av[NS][TM], bv[NS][TN];
 #pragma unroll
         for (int s = 0; s < NS; s++) {
@@ -1171,22 +1188,76 @@ __global__ void __launch_bounds__(PanelGrid<K>::NT, 1)
 // ---------------------------------------------------------------- LASWP
 // Apply the interchanges piv[r0..r1) in order to columns [col0, col0+ncols)
 // of every limb plane (the deferred part of _swap_rows, _kernels.py:597-608).
+//
+// One thread per (limb plane, column).  The interchanges are applied in
+// chunks of LASWP_HC: a chunk touches at most 2 HC rows -- its own rows
+// [rc, rc+hc) and the pivot rows below them -- and the chunk's net row
+// permutation is composed once per CTA on positions (thread 0, shared
+// memory: position j < HC is row rc+j, position HC+i the pivot row of
+// interchange i where it first occurs), so every thread then moves its
+// column's values with independent loads followed by independent stores --
+// one memory round trip per chunk instead of one per interchange (the serial
+// loop was latency-bound: ~0.6 us per interchange, 150 us for a 256-row
+// block; ncu r2).
+constexpr int LASWP_HC = 32;
+constexpr int LASWP_NT = 128;
 template <int K>
-__global__ void laswp_kernel(View A, int64_t col0, int64_t ncols, const int64_t* piv,
-                             int64_t r0, int64_t r1, const int64_t* status) {
-  int64_t cidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (cidx >= ncols) return;
-  int q = blockIdx.y;
-  double* base = (q < K) ? A.re + q * A.ps : A.im + (q - K) * A.ps;
-  int64_t col = col0 + cidx;
+__global__ void __launch_bounds__(LASWP_NT)
+    laswp_kernel(View A, int64_t col0, int64_t ncols, const int64_t* piv, int64_t r0, int64_t r1,
+                 const int64_t* status) {
+  constexpr int HC = LASWP_HC, NT = LASWP_NT;
+  __shared__ int64_t pv[HC];
+  __shared__ int first[HC];
+  __shared__ int src[2 * HC];
+  const int tid = threadIdx.x;
+  const int64_t cidx = (int64_t)blockIdx.x * NT + tid;
+  const bool live = cidx < ncols;
+  const int q = blockIdx.y;
+  double* base = ((q < K) ? A.re + q * A.ps : A.im + (q - K) * A.ps) + col0 + cidx;
   int64_t rend = r1;
   if (status != nullptr && *status >= 0 && *status < rend) rend = *status;
-  for (int64_t r = r0; r < rend; r++) {
-    int64_t p = piv[r];
-    if (p != r) {
-      double x = base[r * A.ld + col];
-      base[r * A.ld + col] = base[p * A.ld + col];
-      base[p * A.ld + col] = x;
+  for (int64_t rc = r0; rc < rend; rc += HC) {
+    const int hc = (int)min((int64_t)HC, rend - rc);
+    __syncthreads();  // the previous chunk's tables are no longer read
+    if (tid < hc) pv[tid] = piv[rc + tid];
+    if (tid < 2 * HC) src[tid] = tid;
+    __syncthreads();
+    if (tid < hc) {
+      int f = tid;
+      for (int i = tid - 1; i >= 0; i--)
+        if (pv[i] == pv[tid]) f = i;
+      first[tid] = f;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int j = 0; j < hc; j++) {
+        const int64_t p = pv[j];
+        if (p == rc + j) continue;
+        const int b2 = p < rc + hc ? (int)(p - rc) : HC + first[j];
+        const int t = src[j];
+        src[j] = src[b2];
+        src[b2] = t;
+      }
+    }
+    __syncthreads();
+    if (live) {
+      // position -> row: i < HC: rc + i; else the pivot row of interchange i - HC
+      double val[2 * HC];  // registers: both loops are fully unrolled
+#pragma unroll
+      for (int i = 0; i < 2 * HC; i++) {
+        const int sidx = src[i];
+        if (sidx != i) {
+          const int64_t row = sidx < HC ? rc + sidx : pv[sidx - HC];
+          val[i] = base[row * A.ld];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2 * HC; i++) {
+        if (src[i] != i) {
+          const int64_t row = i < HC ? rc + i : pv[i - HC];
+          base[row * A.ld] = val[i];
+        }
+      }
     }
   }
 }
@@ -1514,9 +1585,36 @@ inline void retain_pool() {
   done[dev] = true;
 }
 
+// The grid-wide base panel needs all its CTAs resident at once (it spins on
+// a grid barrier).  A cooperative launch guarantees that, but the hardware
+// runs a cooperative grid only once it can place ALL its CTAs, which beside a
+// trailing-update kernel means draining that kernel's CTAs first (measured:
+// with persistent GEMM CTAs resident the panel did not start until the GEMM
+// had finished).  A plain launch places CTAs as slots free up and cannot
+// deadlock as long as the grids that spin fit the device together: a grid is
+// at most PANEL_GRID_GMAX CTAs of <= 20k registers (3 per SM, 444 slots on
+// 148 SMs), everything else on the device (GEMM tiles, S updates) retires on
+// its own.  So ONE factorization per device at a time -- the first to claim
+// the device's slot -- uses plain launches; any other concurrent caller keeps
+// the cooperative launch.  The slot is released by a host callback once the
+// claiming call's stream work has drained.
+inline std::atomic<int>& panel_slot(int dev) {
+  static std::atomic<int> slots[64];
+  return slots[dev & 63];
+}
+inline bool& panel_plain_launch_ok() {
+  static thread_local bool ok = false;
+  return ok;
+}
+inline void CUDART_CB panel_slot_release(void* p) {
+  static_cast<std::atomic<int>*>(p)->fetch_sub(1);
+}
+
 // The lookahead schedule's high-priority side stream and its two events,
 // released on every exit path (a failed launch throws LaunchError mid-loop).
 struct SideStream {
+  cudaStream_t main = nullptr;  // set by the driver: the stream whose drain releases the slot
+  std::atomic<int>* slot = nullptr;
   cudaStream_t sp = nullptr;
   cudaStream_t sh = nullptr;  // helper launches of the capped trailing update
   cudaEvent_t ev_narrow = nullptr, ev_panel = nullptr, ev_queue = nullptr, ev_helper = nullptr;
@@ -1532,8 +1630,34 @@ struct SideStream {
       release();
       throw LaunchError{"side stream / event creation"};
     }
+    static const bool plain = [] {
+      const char* e = getenv("MPC_PANEL_COOP");
+      return !(e && e[0] == '1');
+    }();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (plain) {
+      slot = &panel_slot(dev);
+      if (slot->fetch_add(1) == 0) {
+        panel_plain_launch_ok() = true;
+      } else {
+        slot->fetch_sub(1);
+        slot = nullptr;
+      }
+    }
   }
-  ~SideStream() { release(); }
+  ~SideStream() {
+    if (slot != nullptr) {
+      panel_plain_launch_ok() = false;
+      // after everything this call enqueued (the last panel joins `main`)
+      if (main == nullptr || cudaLaunchHostFunc(main, panel_slot_release, slot) != cudaSuccess) {
+        cudaGetLastError();
+        cudaDeviceSynchronize();
+        slot->fetch_sub(1);
+      }
+    }
+    release();
+  }
   SideStream(const SideStream&) = delete;
   SideStream& operator=(const SideStream&) = delete;
   void release() {
@@ -1637,10 +1761,27 @@ struct Ops {
     // K=3,4: 2 CTAs/SM (register cap 128) measured best for config 3
     // (TD 1.13 s / QD 2.31 s vs 1.39 / 3.14 s at 1 CTA/SM; 128-thread tiles
     // in between -- profiles/r1_cfg3_tdqd.txt)
-    if constexpr (K >= 5)  // verification kernels: registers over occupancy
+    if constexpr (K >= 5) {  // verification kernels: registers over occupancy
       launch_cfg<MODE, BM, BN, BK, TM, TN, 1>(g, st, cls, ops);
-    else
+    } else if constexpr ((K == 3 || K == 4) && !ModeInfo<MODE>::CHAINED) {
+      // TD / QD: the kernel is latency-bound on the renorm dependency chains
+      // (ncu r2: "wait" is the top stall at 16 warps / SM), and with the
+      // accumulators in local memory it fits 62 / 76 registers without
+      // spills: 4 (3) CTAs per SM instead of 2 (MPC_TDQD_MINB for the A/B)
+      static const int minb = [] {
+        const char* e = getenv("MPC_TDQD_MINB");
+        const int v = e ? atoi(e) : 4;
+        return v >= 2 && v <= 4 ? v : 4;
+      }();
+      if (minb == 4)
+        launch_cfg<MODE, BM, BN, BK, TM, TN, 4>(g, st, cls, ops);
+      else if (minb == 3)
+        launch_cfg<MODE, BM, BN, BK, TM, TN, 3>(g, st, cls, ops);
+      else
+        launch_cfg<MODE, BM, BN, BK, TM, TN, 2>(g, st, cls, ops);
+    } else {
       launch_cfg<MODE, BM, BN, BK, TM, TN, 2>(g, st, cls, ops);
+    }
   }
 
   static void rgemm(int64_t m, int64_t n, int64_t l, View a, View b, View c, cudaStream_t st) {
@@ -1715,9 +1856,9 @@ struct Ops {
   static void laswp(View A, int64_t col0, int64_t ncols, const int64_t* piv, int64_t r0,
                     int64_t r1, cudaStream_t st, const int64_t* status) {
     if (ncols <= 0 || r1 <= r0) return;
-    dim3 grid(cdiv_u(ncols, 128), 2 * K);
+    dim3 grid(cdiv_u(ncols, LASWP_NT), 2 * K);
     int tok_ = prof_begin(PC_LASWP, 0.0, st);
-    laswp_kernel<K><<<grid, 128, 0, st>>>(A, col0, ncols, piv, r0, r1, status);
+    laswp_kernel<K><<<grid, LASWP_NT, 0, st>>>(A, col0, ncols, piv, r0, r1, status);
     prof_end(tok_, st);
     check_launch("laswp_kernel");
   }
@@ -1823,9 +1964,11 @@ struct Ops {
         double ops = 0.0;
         for (int64_t j = c0; j < cend; j++) ops += (double)(n - j - 1) * (double)(cend - j - 1);
         int tok_ = prof_begin(PC_PANEL, ops * OpModel<K>::upd(use3m), st);
-        cudaLaunchCooperativeKernel(
-            tpr == 2 ? (void*)panel_grid_kernel<K, 2> : (void*)panel_grid_kernel<K, 1>,
-            dim3((unsigned)G), dim3(NT), args, 0, st);
+        void* kern = tpr == 2 ? (void*)panel_grid_kernel<K, 2> : (void*)panel_grid_kernel<K, 1>;
+        if (panel_plain_launch_ok())  // this call owns the device's slot (see panel_slot)
+          cudaLaunchKernel(kern, dim3((unsigned)G), dim3(NT), args, 0, st);
+        else
+          cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(NT), args, 0, st);
         prof_end(tok_, st);
         check_launch("panel_grid_kernel");
         return;
@@ -1920,12 +2063,28 @@ struct Ops {
 
   // CTAs of the trailing update's first (capped) launch while the next panel
   // is factored beside it (MPC_GEMM_CAP; 0 = one uncapped launch)
-  static int gemm_cap() {
+  // (unset: automatic, see gemm_cap_for; 0: never; N: always N CTAs)
+  static int gemm_cap_env() {
     static int c = [] {
       const char* e = getenv("MPC_GEMM_CAP");
-      return e ? atoi(e) : 0;
+      return e ? atoi(e) : -1;
     }();
     return c;
+  }
+  // Automatic rule (DD): cap the update at 260 of the 296 CTA slots when the
+  // next panel is not comfortably hidden behind it -- estimated update time
+  // under five times the estimated panel time (panel: ~16 us per column of
+  // dependent latency + its chained updates at ~14 T op/s).  Measured on one
+  // B200: config 2 196 -> 190 ms; config 4 only reaches the rule in its last
+  // steps (profiles/r2_gemm_cap_ab.txt; capping every step costs it 3%).
+  static int gemm_cap_for(bool use3m, int64_t rows, int64_t kw, int64_t cols, int64_t kw2) {
+    const int e = gemm_cap_env();
+    if (e >= 0) return e;
+    if constexpr (K != 2) return 0;
+    const double rest_ms = (double)rows * (double)kw * (double)cols *
+                           (use3m ? 3.0 : 4.0) * OpModel<K>::real_mac / 16.5e9;
+    const double panel_ms = 0.016 * (double)kw2 + 4.6e-9 * (double)rows * (double)kw2 * (double)kw2;
+    return rest_ms < 5.0 * panel_ms ? 260 : 0;
   }
 
   // lu._factor (lu.py:129-163) with depth-1 lookahead: while `st` applies
@@ -1936,6 +2095,7 @@ struct Ops {
   static void getrf(bool use3m, View A, int64_t n, int64_t Kp, int64_t* piv, PanelWs ws,
                     cudaStream_t st) {
     SideStream ss;
+    ss.main = st;
     cudaStream_t sp = ss.sp;
     cudaEvent_t ev_narrow = ss.ev_narrow, ev_panel = ss.ev_panel;
     // MPC_TRACE=1: per-step timeline (stderr) -- where the step time goes
@@ -1984,7 +2144,7 @@ struct Ops {
           need(c0 + ch);
           update_cols(use3m, A, n, jb, kw, c0, std::min(n, c0 + ch), piv, ws.status, st);
         }
-      } else if (gemm_cap() > 0 && end + kw2 < n) {
+      } else if (const int cap_req = (end + kw2 < n) ? gemm_cap_for(use3m, n - end, kw, n - end - kw2, kw2) : 0) {
         // capped trailing update: `cap` persistent CTAs claim tiles from a
         // queue, leaving room on every SM for the panel's kernels (which
         // otherwise wait for whole 0.4 - 0.8 ms GEMM CTAs to retire before
@@ -1992,7 +2152,7 @@ struct Ops {
         // helper launch on the same queue restores full occupancy
         const int64_t c0 = end + kw2;
         const int full = 2 * (int)sm_count();
-        const int cap = std::min(gemm_cap(), full);
+        const int cap = std::min(cap_req, full);
         laswp(A, c0, n - c0, piv, jb, end, st, ws.status);
         trsm(use3m, kw, n - c0, A.sub(jb, jb), A.sub(jb, c0), st, ws.status);
         cudaMemsetAsync(ws.tile_ctr, 0, sizeof(unsigned), st);
