@@ -13,7 +13,7 @@ Writes tests/golden/cfg4.json: per input the pivots, SHA-256 of the packed
 factor planes (all planes together and one per limb plane), the right-hand
 side digest and the oracle solve's x digest and forward error.
 
-    python oracle/gen_cfg4.py [uniform] [ill]      # ~1-2 h each at 8 cores
+    python oracle/gen_cfg4.py [uniform] [ill] [--out file]   # ~1 h (16 cores) - 3 h (8 cores) each
 """
 
 import hashlib
@@ -77,8 +77,8 @@ def run(variant):
     return rec
 
 
-def main(variants):
-    path = os.path.join(GOLD, "cfg4.json")
+def main(variants, path=None):
+    path = path or os.path.join(GOLD, "cfg4.json")
     res = {"generator": "oracle/gen_cfg4.py (CPU oracle, pinned to the reference)",
            "cases": []}
     if os.path.exists(path):
@@ -93,4 +93,10 @@ def main(variants):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["uniform", "ill"])
+    args = sys.argv[1:]
+    out = None
+    if "--out" in args:  # e.g. a second machine: merge its case into tests/golden/cfg4.json afterwards
+        i = args.index("--out")
+        out = args[i + 1]
+        del args[i:i + 2]
+    main(args or ["uniform", "ill"], out)

@@ -1613,7 +1613,12 @@ inline void CUDART_CB panel_slot_release(void* p) {
 // The lookahead schedule's high-priority side stream and its two events,
 // released on every exit path (a failed launch throws LaunchError mid-loop).
 struct SideStream {
-  cudaStream_t main = nullptr;  // set by the driver: the stream whose drain releases the slot
+  cudaStream_t main = nullptr;  // set by the driver (set_main): the stream whose drain releases the slot
+  bool has_main = false;        // (the legacy default stream is a null handle)
+  void set_main(cudaStream_t s) {
+    main = s;
+    has_main = true;
+  }
   std::atomic<int>* slot = nullptr;
   cudaStream_t sp = nullptr;
   cudaStream_t sh = nullptr;  // helper launches of the capped trailing update
@@ -1650,7 +1655,7 @@ struct SideStream {
     if (slot != nullptr) {
       panel_plain_launch_ok() = false;
       // after everything this call enqueued (the last panel joins `main`)
-      if (main == nullptr || cudaLaunchHostFunc(main, panel_slot_release, slot) != cudaSuccess) {
+      if (!has_main || cudaLaunchHostFunc(main, panel_slot_release, slot) != cudaSuccess) {
         cudaGetLastError();
         cudaDeviceSynchronize();
         slot->fetch_sub(1);
@@ -1816,10 +1821,12 @@ struct Ops {
                               : (double)m * (double)l * (double)n * (use3m ? 3.0 : 4.0) *
                                     OpModel<K>::real_mac;
     if (use3m)
-      launch_cfg<MODE_G3, BM, BN, BK, TM, TN, 2>(g, st, PC_GEMM, ops, ctas);
+      launch_cfg<MODE_G3, BM, BN, BK, TM, TN, QMINB>(g, st, PC_GEMM, ops, ctas);
     else
-      launch_cfg<MODE_G4, BM, BN, BK, TM, TN, 2>(g, st, PC_GEMM, ops, ctas);
+      launch_cfg<MODE_G4, BM, BN, BK, TM, TN, QMINB>(g, st, PC_GEMM, ops, ctas);
   }
+  // resident CTAs per SM of the queued (persistent) update
+  static constexpr int QMINB = (K == 3 || K == 4) ? 4 : 2;
 
   // chained update C -= L (x) U, each element's subtractions in column order
   static void supdate(bool use3m, int64_t m, int64_t kb, int64_t l, View L, View U, View C,
@@ -2071,20 +2078,28 @@ struct Ops {
     }();
     return c;
   }
-  // Automatic rule (DD): cap the update at 260 of the 296 CTA slots when the
-  // next panel is not comfortably hidden behind it -- estimated update time
-  // under five times the estimated panel time (panel: ~16 us per column of
-  // dependent latency + its chained updates at ~14 T op/s).  Measured on one
-  // B200: config 2 196 -> 190 ms; config 4 only reaches the rule in its last
-  // steps (profiles/r2_gemm_cap_ab.txt; capping every step costs it 3%).
+  // Automatic rule: cap the update at 7/8 of the CTA slots when the next
+  // panel is not comfortably hidden behind it -- estimated update time under
+  // five times the estimated panel time (panel: dependent latency per column
+  // + its chained updates; constants measured on one B200: 16 us / column,
+  // updates at 14 T op/s, GEMM at 16.5).  Config 2: 196 -> 190 ms; config 4
+  // only reaches the rule in its last steps (capping every step costs it 3%:
+  // profiles/r2_gemm_cap_ab.txt).
   static int gemm_cap_for(bool use3m, int64_t rows, int64_t kw, int64_t cols, int64_t kw2) {
     const int e = gemm_cap_env();
     if (e >= 0) return e;
+    // TD / QD: measured no gain (config 3: 590 vs 598 ms, 1118 vs 1153 ms with
+    // the cap) -- their panels are bound by the expansion arithmetic's own
+    // latency, not by waiting for CTA slots -- so the rule is DD only
     if constexpr (K != 2) return 0;
-    const double rest_ms = (double)rows * (double)kw * (double)cols *
-                           (use3m ? 3.0 : 4.0) * OpModel<K>::real_mac / 16.5e9;
-    const double panel_ms = 0.016 * (double)kw2 + 4.6e-9 * (double)rows * (double)kw2 * (double)kw2;
-    return rest_ms < 5.0 * panel_ms ? 260 : 0;
+    constexpr double col_us = 16.0, gemm_tops = 16.5, supd_tops = 14.0;
+    const double rest_ms = (double)rows * (double)kw * (double)cols * (use3m ? 3.0 : 4.0) *
+                           OpModel<K>::real_mac / (gemm_tops * 1e9);
+    const double panel_ms = col_us * 1e-3 * (double)kw2 +
+                            0.485 * (double)rows * (double)kw2 * (double)kw2 *
+                                OpModel<K>::upd(use3m) / (supd_tops * 1e9);
+    const int full = QMINB * (int)sm_count();
+    return rest_ms < 5.0 * panel_ms ? full - full / 8 : 0;
   }
 
   // lu._factor (lu.py:129-163) with depth-1 lookahead: while `st` applies
@@ -2095,7 +2110,7 @@ struct Ops {
   static void getrf(bool use3m, View A, int64_t n, int64_t Kp, int64_t* piv, PanelWs ws,
                     cudaStream_t st) {
     SideStream ss;
-    ss.main = st;
+    ss.set_main(st);
     cudaStream_t sp = ss.sp;
     cudaEvent_t ev_narrow = ss.ev_narrow, ev_panel = ss.ev_panel;
     // MPC_TRACE=1: per-step timeline (stderr) -- where the step time goes
@@ -2151,7 +2166,7 @@ struct Ops {
         // each of their ~300 dependent launches); once the panel is done a
         // helper launch on the same queue restores full occupancy
         const int64_t c0 = end + kw2;
-        const int full = 2 * (int)sm_count();
+        const int full = QMINB * (int)sm_count();
         const int cap = std::min(cap_req, full);
         laswp(A, c0, n - c0, piv, jb, end, st, ws.status);
         trsm(use3m, kw, n - c0, A.sub(jb, jb), A.sub(jb, c0), st, ws.status);

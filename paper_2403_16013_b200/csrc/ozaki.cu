@@ -506,7 +506,7 @@ int64_t mpc_getrf_ozaki(int k, int method, int64_t n, int64_t K, double* re, dou
                            A.sub(end, c0), 1, d, mpc::resolve_width(k, kw, split_bits), s);
     };
     mpc::SideStream ss;
-    ss.main = st;
+    ss.set_main(st);
     cudaStream_t sp = ss.sp;
     cudaEvent_t ev_narrow = ss.ev_narrow, ev_panel = ss.ev_panel;
     // MPC_TRACE=1: per-step timeline on stderr (as mpc_getrf)

@@ -696,7 +696,7 @@ void launch(const Params& P, cudaStream_t st, double ops) {
 // the Ozaki kernel): one CTA per SM, one thread issuing back-to-back
 // tcgen05.mma.kind::i8 M=128 N=256 K=32 from a resident 12 KB smem tile into
 // two TMEM accumulators; int8 ops = 2 * 128 * 256 * 32 per MMA.
-__global__ void __launch_bounds__(128, 1) int8_peak_kernel(int iters, int* sink) {
+__global__ void __launch_bounds__(128, 1) int8_peak_kernel(int iters, int* sink, int ncols = 256) {
   __shared__ __align__(128) int8_t tile[BM * 32 + 256 * 32];
   __shared__ __align__(8) uint64_t done;
   __shared__ uint32_t tmem_slot;
@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(128, 1) int8_peak_kernel(int iters, int* sink)
     const uint64_t ad = ((uint64_t)hi << 32) | (((uint32_t)(BM * 16) >> 4) << 16) | ((s >> 4) & 0x3FFFu);
     const uint64_t bd = ((uint64_t)hi << 32) | (((uint32_t)(256 * 16) >> 4) << 16) |
                         (((s + BM * 32) >> 4) & 0x3FFFu);
-    constexpr uint32_t ID = make_idesc(256, true, true);
+    const uint32_t ID = make_idesc(ncols, true, true);
     if (elect_one()) {
       for (int it = 0; it < iters; it++) mma_i8(tmem + (uint32_t)((it & 1) * 256), ad, bd, ID, 1u);
       mma_commit(&done);
@@ -853,17 +853,27 @@ bool ozaki_tc_rgemm(int k, int64_t m, int64_t n, int64_t l, View A, View B, View
 
 }  // namespace mpc
 
+// MMA N for the microbenchmark: 256 (the roofline denominator) unless
+// MPC_INT8_PEAK_N says otherwise (diagnostics: the Ozaki kernel issues N = 144
+// / 96 MMAs, tools/probe_int8_n.py)
+static int int8_peak_n() {
+  const char* e = getenv("MPC_INT8_PEAK_N");
+  const int v = e ? atoi(e) : 256;
+  return (v >= 16 && v <= 256 && v % 16 == 0) ? v : 256;
+}
+
 extern "C" double mpc_int8_peak(int iters, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  const int ncols = int8_peak_n();
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  mpc::otc::int8_peak_kernel<<<sms, 128, 0, st>>>(iters / 10 + 1, nullptr);  // warm-up
+  mpc::otc::int8_peak_kernel<<<sms, 128, 0, st>>>(iters / 10 + 1, nullptr, ncols);  // warm-up
   cudaEventRecord(a, st);
-  mpc::otc::int8_peak_kernel<<<sms, 128, 0, st>>>(iters, nullptr);
+  mpc::otc::int8_peak_kernel<<<sms, 128, 0, st>>>(iters, nullptr, ncols);
   cudaEventRecord(b, st);
   cudaEventSynchronize(b);
   float t = 0.f;
@@ -871,6 +881,6 @@ extern "C" double mpc_int8_peak(int iters, void* stream) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   if (cudaGetLastError() != cudaSuccess || t <= 0.f) return -1.0;
-  const double ops = (double)sms * (double)iters * 2.0 * mpc::otc::BM * 256.0 * 32.0;
+  const double ops = (double)sms * (double)iters * 2.0 * mpc::otc::BM * (double)ncols * 32.0;
   return ops / (t * 1e-3);  // INT8 tensor-core ops per second
 }

@@ -406,3 +406,88 @@ def test_golden_max_rel_err():
     x.re[0] = [1.0, 0.0, 2.0]
     with pytest.raises(ValueError, match="zero true component at index 1"):
         mp.max_rel_err(x, x)
+
+
+# ------------------------------------- grid-wide base panel: cross-CTA cases
+
+def _small_int_matrix(rng, n, k):
+    """Entries are small integers (exactly representable sums and many exact
+    magnitude ties), so pivot ties occur between rows owned by different CTAs
+    of the base-panel grid."""
+    re = np.zeros((k, n, n))
+    im = np.zeros((k, n, n))
+    re[0] = rng.integers(-3, 4, size=(n, n)).astype(np.float64)
+    im[0] = rng.integers(-3, 4, size=(n, n)).astype(np.float64)
+    return re, im
+
+
+@pytest.mark.parametrize("k,n,K", [(2, 700, 64), (2, 1500, 256), (3, 600, 32)])
+def test_grid_panel_ties_across_ctas_vs_oracle(orc, k, n, K):
+    """Exact |Re|+|Im| ties between rows held by different CTAs (several
+    hundred rows apart) must resolve to the lower current position, as the
+    reference's first-strictly-greater scan does -- pivots and factors bit
+    for bit against the oracle."""
+    rng = np.random.default_rng(1000 * k + n)
+    re, im = _small_int_matrix(rng, n, k)
+    # duplicate rows far apart (distinct CTAs of the grid): identical candidates
+    for a, b in ((3, n - 2), (17, n // 2 + 5), (n // 3, n - 9)):
+        re[:, b, :] = re[:, a, :]
+        im[:, b, :] = im[:, a, :]
+    re[0] += np.eye(n) * 0.5  # keep it nonsingular without destroying the ties
+    fr, fi, piv, st = orc.factor(re, im, K, "3m")
+    if st >= 0:
+        with pytest.raises(mp.SingularMatrixError, match=f"column {st}"):
+            mp.lu_blocked(pc(re, im), K)
+        return
+    f = mp.lu_blocked(pc(re, im), K)
+    assert np.array_equal(f.pivots, piv)
+    assert beq(f.packed.re_plane.data, fr), first_diff(f.packed.re_plane.data, fr)
+    assert beq(f.packed.im_plane.data, fi)
+
+
+def test_grid_panel_late_singular_vs_oracle(orc):
+    """A matrix that becomes singular deep inside a multi-CTA panel: the
+    reported column equals the reference's (lu_panel returns j,
+    _kernels.py:622-624)."""
+    k, n, K = 2, 640, 128
+    rng = np.random.default_rng(99)
+    re, im = problems.lu_matrix(n, k, 5)
+    # an exactly zero column stays exactly zero under the elimination
+    re[:, :, 301] = 0.0
+    im[:, :, 301] = 0.0
+    fr, fi, piv, st = orc.factor(re, im, K, "3m")
+    assert st == 301
+    with pytest.raises(mp.SingularMatrixError, match="column 301"):
+        mp.lu_blocked(pc(re, im), K)
+    del rng, fr, fi, piv
+
+
+@pytest.mark.parametrize("k,n,K", [(2, 2000, 256), (3, 700, 64)])
+def test_panel_implementations_agree_and_repeat(k, n, K):
+    """compute-sanitizer is not available on the GPU pool, so the cross-CTA
+    protocols (grid barrier + published slots, cluster barriers + DSMEM,
+    last-block atomics, the capped tile-queue update) are checked the other
+    way round: every implementation and launch mode must produce the SAME
+    bits, and the same bits on every repetition (a race in any of them shows
+    up as a digest that differs between modes or runs)."""
+    import subprocess
+    import sys
+
+    from testpaths import ROOT as root
+
+    modes = [{}, {"MPC_PANEL_TPR": "1"}, {"MPC_PANEL_COOP": "1"}, {"MPC_PANEL": "cluster"},
+             {"MPC_PANEL": "launches"}, {"MPC_GEMM_CAP": "200"}, {"MPC_GEMM_CAP": "0"}]
+    digests = set()
+    for extra in modes:
+        env = dict(os.environ)
+        for key in ("MPC_PANEL", "MPC_PANEL_TPR", "MPC_PANEL_COOP", "MPC_GEMM_CAP"):
+            env.pop(key, None)
+        env.update(extra)
+        out = subprocess.run([sys.executable, os.path.join(root, "tools", "lu_digest.py"),
+                              str(n), str(K), str(k), "3"], env=env, capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, (extra, out.stderr[-2000:])
+        lines = out.stdout.split()
+        assert len(lines) == 3 and len(set(lines)) == 1, (extra, lines)
+        digests.add(lines[0])
+    assert len(digests) == 1, digests

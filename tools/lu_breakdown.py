@@ -1,5 +1,5 @@
 """Per-class time breakdown (prof summary) of one complex DD LU at n x n:
-python tools/lu_breakdown.py n K [blocked|ozaki]"""
+python tools/lu_breakdown.py n K [blocked|ozaki] [k]"""
 import os
 import sys
 
@@ -12,7 +12,7 @@ n, K = int(sys.argv[1]), int(sys.argv[2])
 kind = sys.argv[3] if len(sys.argv) > 3 else "ozaki"
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(5)
-k = 2
+k = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 re0 = torch.zeros((k, n, n), dtype=torch.float64, device=dev)
 im0 = torch.zeros_like(re0)
 re0[0] = torch.rand((n, n), generator=g, device=dev, dtype=torch.float64) * 2 - 1
