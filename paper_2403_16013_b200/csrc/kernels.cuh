@@ -844,9 +844,14 @@ struct PanelGrid {
   static_assert(K + 1 + 2 * K * W <= PANEL_GRID_SLOT, "slot too small");
 };
 
-MPC_DI unsigned ld_acquire_u32(const unsigned* p) {
+// Poll of the grid-barrier word.  Relaxed (L2) loads, NOT ld.acquire: an
+// acquire load invalidates the SM's L1 on every poll (CCTL.IVALL, ~40 polls
+// per barrier in the ncu capture), and the rows live in L1-resident local
+// memory.  Everything read after the barrier is read with ld.cg (L2), after
+// the writers' __threadfence() + arrival, so no L1 line can be stale.
+MPC_DI unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -909,7 +914,6 @@ __global__ void __launch_bounds__(PanelGrid<K>::NT, 1)
     }
   }
   unsigned epoch = 0;
-  bool singular = false;
   for (int q = 0; q < w; q++) {
     const int par = q & 1;
     const int64_t jj = c0 + q;
@@ -1038,7 +1042,7 @@ __global__ void __launch_bounds__(PanelGrid<K>::NT, 1)
     if (G > 1) {
       epoch++;
       if (tid == 0)
-        while (ld_acquire_u32(&gbar[0]) < epoch * G) {
+        while (ld_relaxed_u32(&gbar[0]) < epoch * G) {
         }
       __syncthreads();
       // 5. warp 0: the global argmax (same result in every CTA), pivot row to smem
@@ -1084,7 +1088,6 @@ __global__ void __launch_bounds__(PanelGrid<K>::NT, 1)
     const int64_t P = pick_s[par];
     if (P < 0) {  // lu_panel returns jj (_kernels.py:622-624); uniform across the grid
       if (blockIdx.x == 0 && tid == 0 && *status < 0) *status = jj;
-      singular = true;
       break;
     }
     if (blockIdx.x == 0 && tid == 0) piv[jj] = P;
@@ -1165,7 +1168,6 @@ __global__ void __launch_bounds__(PanelGrid<K>::NT, 1)
       }
     }
   }
-  (void)singular;
   // rows to their final positions (every CTA loaded its rows before its first
   // arrival, so no row is overwritten before its owner has read it)
   if (valid && sub == 0) {
@@ -1268,31 +1270,31 @@ __global__ void __launch_bounds__(LASWP_NT)
 // step s lane s's value is final (all its subtractions s' < s are done); it
 // is broadcast by shuffle and every lane r > s applies x_r -= cmul(L_rs, x_s).
 // Each x_r therefore receives exactly the reference's chain (s ascending).
-constexpr int TRSM_BASE_MAX = 16;
-template <int K>
+// TB = rows of the diagonal block = lanes per column (16 or 32).
+template <int K, int TB>
 MPC_DI Exp<K> shfl_exp(const Exp<K>& v, int src) {
   Exp<K> o;
 #pragma unroll
-  for (int q = 0; q < K; q++) o.c[q] = __shfl_sync(0xffffffffu, v.c[q], src, TRSM_BASE_MAX);
+  for (int q = 0; q < K; q++) o.c[q] = __shfl_sync(0xffffffffu, v.c[q], src, TB);
   return o;
 }
 
-template <int K>
+template <int K, int TB>
 __global__ void trsm_diag_kernel(View L, View X, int64_t kb, int64_t M, int use3m,
                                  const int64_t* status) {
   if (status != nullptr && *status >= 0) return;
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int r = (int)(gid % TRSM_BASE_MAX);
-  int64_t col = gid / TRSM_BASE_MAX;
-  bool live = col < M && r < kb;  // whole 16-lane groups share a column
+  int r = (int)(gid % TB);
+  int64_t col = gid / TB;
+  bool live = col < M && r < kb;  // whole TB-lane groups share a column
   Exp<K> xr = exp_zero<K>(), xi = exp_zero<K>();
   if (live) {
     xr = ldexp_<K>(X.re + r * X.ld + col, X.ps);
     xi = ldexp_<K>(X.im + r * X.ld + col, X.ps);
   }
   for (int s = 0; s + 1 < (int)kb; s++) {
-    Exp<K> yr = shfl_exp<K>(xr, s);
-    Exp<K> yi = shfl_exp<K>(xi, s);
+    Exp<K> yr = shfl_exp<K, TB>(xr, s);
+    Exp<K> yi = shfl_exp<K, TB>(xi, s);
     if (live && r > s) {
       Exp<K> lr = ldexp_<K>(L.re + r * L.ld + s, L.ps);
       Exp<K> li = ldexp_<K>(L.im + r * L.ld + s, L.ps);
@@ -1870,15 +1872,29 @@ struct Ops {
     check_launch("laswp_kernel");
   }
 
-  static constexpr int TRSM_BASE = TRSM_BASE_MAX;
+  // rows of a diagonal block handled by one trsm_diag_kernel launch: 16, or
+  // 32 (half the launches of the recursion, twice the serial steps per
+  // launch; MPC_TRSM_BASE for the A/B)
+  static int trsm_base() {
+    static int b = [] {
+      const char* e = getenv("MPC_TRSM_BASE");
+      return e && atoi(e) == 32 ? 32 : 16;
+    }();
+    return b;
+  }
   // L (kb x kb, unit lower, strictly-lower part read) and X (kb x M) views
   static void trsm(bool use3m, int64_t kb, int64_t M, View L, View X, cudaStream_t st,
                    const int64_t* status) {
     if (kb <= 1 || M <= 0) return;
-    if (kb <= TRSM_BASE) {
+    const int TB = trsm_base();
+    if (kb <= TB) {
       int tok_ = prof_begin(PC_TRSM, (double)M * (double)(kb * (kb - 1) / 2) * OpModel<K>::upd(use3m), st);
-      trsm_diag_kernel<K><<<cdiv_u(M * TRSM_BASE_MAX, 128), 128, 0, st>>>(L, X, kb, M,
-                                                                            use3m ? 1 : 0, status);
+      if (TB == 32)
+        trsm_diag_kernel<K, 32><<<cdiv_u(M * 32, 128), 128, 0, st>>>(L, X, kb, M, use3m ? 1 : 0,
+                                                                    status);
+      else
+        trsm_diag_kernel<K, 16><<<cdiv_u(M * 16, 128), 128, 0, st>>>(L, X, kb, M, use3m ? 1 : 0,
+                                                                    status);
       prof_end(tok_, st);
       check_launch("trsm_diag_kernel");
       return;
