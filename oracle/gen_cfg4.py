@@ -77,6 +77,56 @@ def run(variant):
     return rec
 
 
+def run_staged(variant, stage, state, split_panels=6):
+    """The same record in two stages for machines with a per-job time limit:
+    stage A runs the first `split_panels` panels (about half the work) and
+    saves the matrix, piv and the partial record under `state`; stage B loads
+    them, finishes the factorization and the solve."""
+    ill = variant == "ill"
+    f_re, f_im, f_piv, f_rec = (os.path.join(state, x) for x in
+                                ("re.npy", "im.npy", "piv.npy", "rec.json"))
+    split = split_panels * K
+    if stage == "A":
+        os.makedirs(state, exist_ok=True)
+        re, im = problems.lu_matrix(N, k, 1, ill_conditioned=ill)
+        rec = {"variant": variant, "n": N, "K": K, "k": k, "method": "3m", "seed": 1,
+               "input_digest": digest(re, im), "threads": os.cpu_count(), "staged": split}
+        xr, xi = problems.x_true(N, k)
+        br, bi = oracle.cgemm(re, im, xr.reshape(k, N, 1), xi.reshape(k, N, 1), "4m")
+        np.save(os.path.join(state, "b.npy"), np.array([br[:, :, 0], bi[:, :, 0]]))
+        piv = np.arange(N, dtype=np.int64)
+        t0 = time.perf_counter()
+        st = oracle.factor_range(re, im, piv, K, "3m", 0, split)
+        rec["seconds_A"] = time.perf_counter() - t0
+        assert st == -1, st
+        np.save(f_re, re)
+        np.save(f_im, im)
+        np.save(f_piv, piv)
+        json.dump(rec, open(f_rec, "w"))
+        print("stage A done", rec["seconds_A"], flush=True)
+        return None
+    rec = json.load(open(f_rec))
+    re, im, piv = np.load(f_re), np.load(f_im), np.load(f_piv)
+    b = np.load(os.path.join(state, "b.npy"))
+    br, bi = b[0].copy(), b[1].copy()
+    rec["b_digest"] = digest(np.array([br, bi]))
+    t0 = time.perf_counter()
+    st = oracle.factor_range(re, im, piv, K, "3m", split, N)
+    rec["seconds_B"] = time.perf_counter() - t0
+    rec["seconds"] = rec["seconds_A"] + rec["seconds_B"]
+    rec["status"] = st
+    rec["pivots"] = [int(p) for p in piv]
+    rec["digest"] = digest(re, im)
+    rec["digest_planes"] = [digest(re[c]) for c in range(k)] + [digest(im[c]) for c in range(k)]
+    t0 = time.perf_counter()
+    x_r, x_i = oracle.solve_fb(re, im, piv, br, bi, "3m")
+    rec["solve_seconds"] = time.perf_counter() - t0
+    rec["x_digest"] = digest(x_r, x_i)
+    rec["fwd_err"] = fwd_err(x_r, x_i)
+    print("stage B done", rec["seconds_B"], rec["fwd_err"], flush=True)
+    return rec
+
+
 def main(variants, path=None):
     path = path or os.path.join(GOLD, "cfg4.json")
     res = {"generator": "oracle/gen_cfg4.py (CPU oracle, pinned to the reference)",
@@ -99,4 +149,19 @@ if __name__ == "__main__":
         i = args.index("--out")
         out = args[i + 1]
         del args[i:i + 2]
+    if "--stage" in args:  # python oracle/gen_cfg4.py ill --stage A|B --state DIR [--out file]
+        i = args.index("--stage")
+        stage = args[i + 1]
+        del args[i:i + 2]
+        i = args.index("--state")
+        state = args[i + 1]
+        del args[i:i + 2]
+        r = run_staged(args[0], stage, state)
+        if r is not None:
+            path = out or os.path.join(GOLD, "cfg4.json")
+            res = json.load(open(path)) if os.path.exists(path) else {
+                "generator": "oracle/gen_cfg4.py (CPU oracle, pinned to the reference)", "cases": []}
+            res["cases"] = [c for c in res["cases"] if c["variant"] != r["variant"]] + [r]
+            json.dump(res, open(path, "w"))
+        sys.exit(0)
     main(args or ["uniform", "ill"], out)

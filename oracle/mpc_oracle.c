@@ -552,10 +552,13 @@ void orc_trsm_ll_unit(int k, int use3m, int64_t K, int64_t M, const double *lre,
 
 /* lu._factor, lu.py:129-163 (in place on re/im; piv preset to arange by the
  * caller, as lu.py:134).  Returns -1 or the singular column. */
-int64_t orc_factor(int k, int use3m, int64_t n, int64_t K, double *re, double *im,
-                   int64_t *piv) {
+/* The panels jb in [jb0, jb1) of lu._factor's loop (jb0 a multiple of K): a
+ * long factorization can be run in stages, the matrix and piv carried over
+ * (oracle/gen_cfg4.py --stage).  orc_factor is the whole range. */
+int64_t orc_factor_range(int k, int use3m, int64_t n, int64_t K, double *re, double *im,
+                         int64_t *piv, int64_t jb0, int64_t jb1) {
     int64_t ps = n * n;
-    for (int64_t jb = 0; jb < n; jb += K) {
+    for (int64_t jb = jb0; jb < n && jb < jb1; jb += K) {
         int64_t kw = (K < n - jb) ? K : n - jb;
         int64_t status = orc_lu_panel(k, use3m, n, re, im, piv, jb, kw);
         if (status >= 0) return status;
@@ -579,6 +582,11 @@ int64_t orc_factor(int k, int use3m, int64_t n, int64_t K, double *re, double *i
         free(pim);
     }
     return -1;
+}
+
+int64_t orc_factor(int k, int use3m, int64_t n, int64_t K, double *re, double *im,
+                   int64_t *piv) {
+    return orc_factor_range(k, use3m, n, K, re, im, piv, 0, n);
 }
 
 /* solve_fb, _kernels.py:708-775 (b overwritten by x; vectors (k, n)) */

@@ -66,6 +66,7 @@ def _load():
         "orc_trsm_ll_unit": (None, [_int, _int, _i64, _i64, _dp, _dp, _i64, _i64, _dp, _dp,
                                     _i64, _i64]),
         "orc_factor": (_i64, [_int, _int, _i64, _i64, _dp, _dp, _i64p]),
+        "orc_factor_range": (_i64, [_int, _int, _i64, _i64, _dp, _dp, _i64p, _i64, _i64]),
         "orc_solve_fb": (None, [_int, _int, _i64, _dp, _dp, _i64p, _dp, _dp]),
         "orc_solve_phases": (None, [_int, _int, _i64, _dp, _dp, _i64p, _dp, _dp, _int]),
         "orc_set_threads": (_int, [_int]),
@@ -252,6 +253,16 @@ def factor(re, im, K, method="3m"):
     st = _load().orc_factor(k, int(method == "3m"), n, K, _d(re), _d(im),
                             piv.ctypes.data_as(_i64p))
     return re, im, piv, int(st)
+
+
+def factor_range(re, im, piv, K, method, jb0, jb1):
+    """Panels jb in [jb0, jb1) of lu._factor IN PLACE on C-contiguous float64
+    planes and an int64 piv (arange before the first stage) -> status."""
+    assert re.flags.c_contiguous and im.flags.c_contiguous and piv.dtype == np.int64
+    k, n, _ = re.shape
+    lib = _load()
+    return int(lib.orc_factor_range(k, int(method == "3m"), n, K, _d(re), _d(im),
+                                    piv.ctypes.data_as(_i64p), jb0, jb1))
 
 
 def solve_fb(re, im, piv, br, bi, method="3m", phases=3):

@@ -1561,6 +1561,11 @@ struct OpModel {
   static constexpr double upd3 = K == 2 ? 173.0 : (K == 3 ? 833.0 : 1323.0);
   static constexpr double upd4 = K == 2 ? 124.0 : (K == 3 ? 780.0 : 1300.0);
   static double upd(bool use3m) { return use3m ? upd3 : upd4; }
+  // the chained "S" update kernel forms the two 3M operand sums once per
+  // STAGED element (cmul3_pre), not once per output element: 3 products + 5
+  // additions per update are what the FP64 pipe executes (charging
+  // 173 overstated the S-class rate by ~30%)
+  static constexpr double upd3_exec = K == 2 ? 133.0 : (K == 3 ? 709.0 : 1149.0);
 };
 
 struct LaunchError {
@@ -1836,7 +1841,7 @@ struct Ops {
     if (m <= 0 || l <= 0 || kb <= 0) return;
     GemmArgs g{m, kb, l, L, U, C, 0, status};
     if (use3m)
-      gemm_launch<MODE_S3>(g, st, PC_SUPD, OpModel<K>::upd3);
+      gemm_launch<MODE_S3>(g, st, PC_SUPD, OpModel<K>::upd3_exec);
     else
       gemm_launch<MODE_S4>(g, st, PC_SUPD, OpModel<K>::upd4);
   }
