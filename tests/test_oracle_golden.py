@@ -137,3 +137,21 @@ def test_cfg0_digests(orc):
         assert st == -1
         assert [int(p) for p in piv] == c["pivots"]
         assert digest(fr, fi) == c["digest"], (c["seed"], c["method"], c["K"])
+
+
+def test_factor_range_stages_equal_whole(orc):
+    """oracle.factor_range (used by oracle/gen_cfg4.py --stage to run the
+    config-4 factorization in two jobs) continues exactly where the previous
+    stage stopped: two stages == one call, bit for bit."""
+    import numpy as np
+
+    from paper_2403_16013_b200 import problems
+
+    re, im = problems.lu_matrix(96, 2, 11)
+    fr, fi, piv, st = orc.factor(re, im, 16, "3m")
+    r2, i2 = re.copy(), im.copy()
+    p2 = np.arange(96, dtype=np.int64)
+    assert orc.factor_range(r2, i2, p2, 16, "3m", 0, 48) == -1
+    assert orc.factor_range(r2, i2, p2, 16, "3m", 48, 96) == -1
+    assert st == -1 and np.array_equal(piv, p2)
+    assert fr.tobytes() == r2.tobytes() and fi.tobytes() == i2.tobytes()
