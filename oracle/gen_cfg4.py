@@ -13,7 +13,8 @@ Writes tests/golden/cfg4.json: per input the pivots, SHA-256 of the packed
 factor planes (all planes together and one per limb plane), the right-hand
 side digest and the oracle solve's x digest and forward error.
 
-    python oracle/gen_cfg4.py [uniform] [ill] [--out file]   # ~1 h (16 cores) - 3 h (8 cores) each
+    python oracle/gen_cfg4.py [uniform] [ill] [--out file]   # measured: ~7 h per input on 8 shared cores
+    python oracle/gen_cfg4.py ill_n8192 --n 8192 [--out file]  # the same workload at n = 8192 (1/8 of the work)
 """
 
 import hashlib
@@ -51,7 +52,7 @@ def fwd_err(xr, xi):
 
 
 def run(variant):
-    ill = variant == "ill"
+    ill = variant.startswith("ill")
     re, im = problems.lu_matrix(N, k, 1, ill_conditioned=ill)
     rec = {"variant": variant, "n": N, "K": K, "k": k, "method": "3m", "seed": 1,
            "input_digest": digest(re, im)}
@@ -77,15 +78,34 @@ def run(variant):
     return rec
 
 
-def run_staged(variant, stage, state, split_panels=6):
-    """The same record in two stages for machines with a per-job time limit:
-    stage A runs the first `split_panels` panels (about half the work) and
-    saves the matrix, piv and the partial record under `state`; stage B loads
-    them, finishes the factorization and the solve."""
-    ill = variant == "ill"
+# panel boundaries of the stages: four stages of about equal work (the work
+# left after panel p is ((32 - p) / 32)^3 of the total)
+STAGE_PANELS = {"A": (0, 3), "B": (3, 7), "C": (7, 12), "D": (12, 1 << 30)}
+
+
+def run_staged(variant, stage, state):
+    """The same record in four stages for machines with a per-job time limit
+    (measured: ~2 h per full-size input on 16 host cores, limit 1 h): stage A
+    builds the input and runs the first panels, every stage saves the matrix
+    and piv under `state`, stage D finishes the factorization and the solve."""
+    ill = variant.startswith("ill")
     f_re, f_im, f_piv, f_rec = (os.path.join(state, x) for x in
                                 ("re.npy", "im.npy", "piv.npy", "rec.json"))
-    split = split_panels * K
+    p0, p1 = STAGE_PANELS[stage]
+    if stage in ("B", "C"):
+        rec = json.load(open(f_rec))
+        re, im, piv = np.load(f_re), np.load(f_im), np.load(f_piv)
+        t0 = time.perf_counter()
+        st = oracle.factor_range(re, im, piv, K, "3m", p0 * K, p1 * K)
+        rec["seconds_" + stage] = time.perf_counter() - t0
+        assert st == -1, st
+        np.save(f_re, re)
+        np.save(f_im, im)
+        np.save(f_piv, piv)
+        json.dump(rec, open(f_rec, "w"))
+        print("stage", stage, "done", rec["seconds_" + stage], flush=True)
+        return None
+    split = p1 * K if stage == "A" else p0 * K
     if stage == "A":
         os.makedirs(state, exist_ok=True)
         re, im = problems.lu_matrix(N, k, 1, ill_conditioned=ill)
@@ -112,8 +132,8 @@ def run_staged(variant, stage, state, split_panels=6):
     rec["b_digest"] = digest(np.array([br, bi]))
     t0 = time.perf_counter()
     st = oracle.factor_range(re, im, piv, K, "3m", split, N)
-    rec["seconds_B"] = time.perf_counter() - t0
-    rec["seconds"] = rec["seconds_A"] + rec["seconds_B"]
+    rec["seconds_D"] = time.perf_counter() - t0
+    rec["seconds"] = sum(rec["seconds_" + x] for x in "ABCD")
     rec["status"] = st
     rec["pivots"] = [int(p) for p in piv]
     rec["digest"] = digest(re, im)
@@ -123,7 +143,7 @@ def run_staged(variant, stage, state, split_panels=6):
     rec["solve_seconds"] = time.perf_counter() - t0
     rec["x_digest"] = digest(x_r, x_i)
     rec["fwd_err"] = fwd_err(x_r, x_i)
-    print("stage B done", rec["seconds_B"], rec["fwd_err"], flush=True)
+    print("stage D done", rec["seconds_D"], rec["fwd_err"], flush=True)
     return rec
 
 
@@ -145,11 +165,15 @@ def main(variants, path=None):
 if __name__ == "__main__":
     args = sys.argv[1:]
     out = None
+    if "--n" in args:  # a smaller instance of the same workload, e.g. ill_n8192 --n 8192
+        i = args.index("--n")
+        N = int(args[i + 1])
+        del args[i:i + 2]
     if "--out" in args:  # e.g. a second machine: merge its case into tests/golden/cfg4.json afterwards
         i = args.index("--out")
         out = args[i + 1]
         del args[i:i + 2]
-    if "--stage" in args:  # python oracle/gen_cfg4.py ill --stage A|B --state DIR [--out file]
+    if "--stage" in args:  # python oracle/gen_cfg4.py ill --stage A|B|C|D --state DIR [--out file]
         i = args.index("--stage")
         stage = args[i + 1]
         del args[i:i + 2]

@@ -257,3 +257,41 @@ def test_factor_inplace_pinned_overlap_ozaki(mp, n, K):
     assert np.array_equal(pp, dp.cpu().numpy())
     assert pr.numpy().tobytes() == dr.cpu().numpy().tobytes()
     assert pi.numpy().tobytes() == di.cpu().numpy().tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,rows,ncols,r0,r1", [(2, 300, 200, 5, 150), (3, 97, 33, 0, 97),
+                                                (2, 1200, 129, 64, 576), (4, 40, 5, 3, 4)])
+def test_laswp_chunked_permutation_vs_sequential(mp, k, rows, ncols, r0, r1):
+    """mpc_laswp (chunks of 32 interchanges composed into one permutation per
+    chunk) against the sequential definition (_swap_rows in order,
+    _kernels.py:597-608): random pivots p >= r with many repeats -- the same
+    pivot row hit by several interchanges of one chunk and of different
+    chunks, pivots inside the chunk, identity interchanges."""
+    from paper_2403_16013_b200 import _lib
+
+    rng = np.random.default_rng(rows * 7 + ncols)
+    re = rng.standard_normal((k, rows, ncols))
+    im = rng.standard_normal((k, rows, ncols))
+    piv = np.arange(rows, dtype=np.int64)
+    hot = rng.integers(r1, rows, size=4) if r1 < rows else np.array([rows - 1])
+    for r in range(r0, r1):
+        u = rng.random()
+        if u < 0.15:
+            piv[r] = r                                   # identity
+        elif u < 0.45:
+            piv[r] = rng.integers(r, min(r + 20, rows))  # nearby (often inside the chunk)
+        elif u < 0.75:
+            piv[r] = max(r, int(rng.choice(hot)))        # a few rows hit again and again
+        else:
+            piv[r] = rng.integers(r, rows)
+    er, ei = re.copy(), im.copy()
+    for r in range(r0, r1):
+        p = piv[r]
+        if p != r:
+            er[:, [r, p], :] = er[:, [p, r], :]
+            ei[:, [r, p], :] = ei[:, [p, r], :]
+    gr, gi = re.copy(), im.copy()
+    _lib.check(_lib.lib().mpc_laswp(k, ncols, _lib.ptr(gr), _lib.ptr(gi), ncols, rows * ncols,
+                                    _lib.ptr(piv), r0, r1, None), "laswp")
+    assert gr.tobytes() == er.tobytes() and gi.tobytes() == ei.tobytes()
