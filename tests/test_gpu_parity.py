@@ -313,12 +313,10 @@ def test_cfg4_lu_digest(variant):
     """BASELINE config 4 (n=16384, K=512, DD, 3M): pivots and per-plane
     digests of the packed factors against the pinned CPU oracle's one-time
     run (oracle/gen_cfg4.py), and the forward error of the GPU solve against
-    the oracle's.  Device path (8 GiB per matrix).  The oracle needs ~7 h per
-    full-size input on this container's 8 cores (and more than the GPU box's
-    per-job limit allows), so the ill-conditioned input is pinned at full
-    block width on half the order (ill_n8192: n=8192, K=512) in addition to
-    the reference's own n=4096 record (test_ill_conditioned_n4096_digest);
-    a variant without a record is skipped."""
+    the oracle's.  Device path (8 GiB per matrix).  Both full-size inputs
+    (uniform: 5.95 h on this container's 8 cores; ill: 2.6 h in four stages
+    on the GPU box's 16 host cores) and the ill-conditioned input at n=8192,
+    K=512; a variant without a record is skipped."""
     import torch
 
     from paper_2403_16013_b200 import device
